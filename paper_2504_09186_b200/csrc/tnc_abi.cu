@@ -1,0 +1,513 @@
+// C-ABI entry points (include/tnc_b200.h) and the contraction planner.
+//
+// tnc_plan_contract realises the reference's contract_pair index map
+// (contract.py:58-117): free_A (A order), common (A order), free_B (B order),
+// result legs free_A ++ free_B (or a caller-given permutation of them).  The
+// device execution differs from the reference's permute-both-then-GEMM:
+//   * the larger operand X goes on the GEMM row side and keeps its own order
+//     of the common legs, so it is consumed in place whenever its legs are
+//     already [free..., common...] (true for most stem tensors);
+//   * the smaller operand Y is gathered to [free_Y, common(X order)];
+//   * the GEMM epilogue writes C straight into the output layout
+//     (free_A ++ free_B, row- or column-oriented), no trailing transpose.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "tnc_common.cuh"
+
+namespace tnc {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+namespace {
+
+struct Leg {
+  int32_t label;
+  int64_t dim;
+  int64_t stride;
+};
+
+struct Operand {
+  std::vector<Leg> free;    // operand's own order
+  std::vector<Leg> common;  // in X's common order
+  bool in_place = false;    // consumable as a [rows, K] matrix without a gather
+  int64_t ld = 0;           // row stride when in place
+  // gather (permute) description when not in place
+  std::vector<int64_t> dims, strides;
+  std::vector<int32_t> perm;
+  int64_t rows = 1;
+};
+
+}  // namespace
+}  // namespace tnc
+
+struct tnc_plan {
+  int32_t dtype;
+  int32_t variant;
+  int32_t b_is_multiplier;
+  int32_t x_is_a;  // row-side operand is A
+  int64_t m, k, n;        // reference TTGT shape (free_A, common, free_B)
+  int64_t rows_x, rows_y; // GEMM rows of X and Y
+  int64_t kp;             // padded K for the tensor-core planes
+  int32_t n_common;
+  tnc::Operand x, y;
+  int64_t ldcm, ldcn;      // C[x, y] strides in the (default-order) result
+  bool custom_out;         // result order is a different permutation
+  std::vector<int64_t> out_perm_dims, out_perm_strides;
+  std::vector<int32_t> out_perm;
+  int32_t out_rank;
+  std::vector<int32_t> out_labels;
+  std::vector<int64_t> out_dims;
+  // workspace layout (bytes)
+  size_t off_x, off_y, off_planes, off_partials, off_tmp, ws_bytes;
+  int32_t k_splits;
+  __int128 multiplies;
+};
+
+namespace tnc {
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
+
+bool checked_mul(int64_t a, int64_t b, int64_t* out) {
+  __int128 r = static_cast<__int128>(a) * b;
+  if (r > static_cast<__int128>(INT64_MAX)) return false;
+  *out = static_cast<int64_t>(r);
+  return true;
+}
+
+int read_desc(const tnc_tensor_desc* d, std::vector<Leg>& legs) {
+  if (!d) TNC_RET(TNC_ERR_INVALID, "null tensor descriptor");
+  if (d->rank < 0 || d->rank > TNC_MAX_RANK) TNC_RET(TNC_ERR_TENSOR, "rank out of range");
+  legs.clear();
+  for (int i = 0; i < d->rank; ++i) {
+    if (d->dims[i] < 1) TNC_RET(TNC_ERR_TENSOR, "dim < 1");
+    for (auto& l : legs)
+      if (l.label == d->labels[i]) TNC_RET(TNC_ERR_TENSOR, "duplicate label in tensor");
+    legs.push_back({d->labels[i], d->dims[i], d->strides[i]});
+  }
+  return TNC_OK;
+}
+
+// Is `legs` (in memory order given by strides) a [free..., common...] matrix
+// with unit-stride K?  free/common are in the order the GEMM enumerates them.
+bool matrix_view(const std::vector<Leg>& free, const std::vector<Leg>& common, int64_t* ld) {
+  int64_t expect = 1;
+  for (int i = static_cast<int>(common.size()) - 1; i >= 0; --i) {
+    if (common[i].dim == 1) continue;
+    if (common[i].stride != expect) return false;
+    expect *= common[i].dim;
+  }
+  const int64_t kk = expect;
+  // free legs: innermost free stride defines ld, then row-major above it
+  int64_t row_stride = -1;
+  int64_t fexpect = -1;
+  for (int i = static_cast<int>(free.size()) - 1; i >= 0; --i) {
+    if (free[i].dim == 1) continue;
+    if (fexpect < 0) {
+      if (free[i].stride < kk) return false;
+      row_stride = free[i].stride;
+      fexpect = free[i].stride;
+    }
+    if (free[i].stride != fexpect) return false;
+    fexpect *= free[i].dim;
+  }
+  *ld = row_stride < 0 ? kk : row_stride;
+  return true;
+}
+
+void build_gather(Operand& op) {
+  // source legs = free then common (each with its stride); output contiguous
+  op.dims.clear();
+  op.strides.clear();
+  op.perm.clear();
+  int idx = 0;
+  for (auto& l : op.free) {
+    op.dims.push_back(l.dim);
+    op.strides.push_back(l.stride);
+    op.perm.push_back(idx++);
+  }
+  for (auto& l : op.common) {
+    op.dims.push_back(l.dim);
+    op.strides.push_back(l.stride);
+    op.perm.push_back(idx++);
+  }
+}
+
+bool tc_eligible(const tnc_plan* p) {
+  return p->dtype == TNC_C64 && p->rows_x >= 128 && p->rows_y >= 32 && p->k >= 32 &&
+         static_cast<__int128>(p->rows_x) * p->rows_y * p->k >= (static_cast<__int128>(1) << 26);
+}
+
+}  // namespace
+}  // namespace tnc
+
+using namespace tnc;
+
+extern "C" {
+
+int tnc_abi_version(void) { return TNC_ABI_VERSION; }
+
+const char* tnc_last_error(void) { return tnc::last_error(); }
+
+int tnc_init(int device) {
+  TNC_CUDA_TRY(cudaSetDevice(device));
+  TNC_CUDA_TRY(cudaFree(nullptr));
+  return TNC_OK;
+}
+
+int tnc_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* smem_optin) {
+  int dev = 0;
+  TNC_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  TNC_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (smem_optin) *smem_optin = prop.sharedMemPerBlockOptin;
+  return TNC_OK;
+}
+
+int tnc_permute(int32_t dtype, int32_t rank, const int64_t* dims, const int64_t* in_strides,
+                const int32_t* perm, const void* in, void* out, void* stream) {
+  if (dtype != TNC_C64 && dtype != TNC_C128) TNC_RET(TNC_ERR_INVALID, "permute: bad dtype");
+  return permute_launch(dtype, rank, dims, in_strides, perm, in, out,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int tnc_axpy(int32_t dtype, int64_t n, const void* x, void* y, void* stream) {
+  return axpy_launch(dtype, n, x, y, static_cast<cudaStream_t>(stream));
+}
+
+int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_t out_rank,
+                      const int32_t* out_labels, int32_t variant, tnc_plan** plan_out) {
+  if (!plan_out) TNC_RET(TNC_ERR_INVALID, "null plan pointer");
+  *plan_out = nullptr;
+  std::vector<Leg> la, lb;
+  TNC_TRY(read_desc(a, la));
+  TNC_TRY(read_desc(b, lb));
+  if (a->dtype != b->dtype) TNC_RET(TNC_ERR_INVALID, "operand dtypes differ");
+  if (a->dtype != TNC_C64 && a->dtype != TNC_C128) TNC_RET(TNC_ERR_INVALID, "bad dtype");
+  std::vector<Leg> free_a, common_a, free_b, common_b;
+  for (auto& l : la) {
+    const Leg* twin = nullptr;
+    for (auto& r : lb)
+      if (r.label == l.label) twin = &r;
+    if (!twin) {
+      free_a.push_back(l);
+    } else {
+      if (twin->dim != l.dim) TNC_RET(TNC_ERR_CONTRACTION, "shared label has mismatched dims");
+      common_a.push_back(l);
+      common_b.push_back(*twin);
+    }
+  }
+  for (auto& r : lb) {
+    bool shared = false;
+    for (auto& l : la) shared |= (l.label == r.label);
+    if (!shared) free_b.push_back(r);
+  }
+  auto* p = new tnc_plan();
+  p->dtype = a->dtype;
+  p->n_common = static_cast<int32_t>(common_a.size());
+  int64_t m = 1, k = 1, n = 1;
+  bool ok = true;
+  for (auto& l : free_a) ok &= checked_mul(m, l.dim, &m);
+  for (auto& l : common_a) ok &= checked_mul(k, l.dim, &k);
+  for (auto& l : free_b) ok &= checked_mul(n, l.dim, &n);
+  int64_t tmp;
+  ok &= checked_mul(m, n, &tmp);
+  if (!ok) {
+    delete p;
+    TNC_RET(TNC_ERR_TENSOR, "contraction extent overflows int64");
+  }
+  p->m = m;
+  p->k = k;
+  p->n = n;
+  p->multiplies = static_cast<__int128>(m) * k * n;
+  // reference multiplier choice (ties resolved by the caller's label strings)
+  p->b_is_multiplier = (k * n > m * k) ? 1 : 0;
+  // row side X = larger operand (ties: A)
+  p->x_is_a = (k * n > m * k) ? 0 : 1;
+  Operand& X = p->x;
+  Operand& Y = p->y;
+  if (p->x_is_a) {
+    X.free = free_a;
+    X.common = common_a;
+    Y.free = free_b;
+    Y.common = common_b;  // already listed in A's common order
+  } else {
+    // common order = B's own order; reorder A's commons accordingly
+    X.free = free_b;
+    Y.free = free_a;
+    for (auto& r : lb)
+      for (size_t i = 0; i < common_b.size(); ++i)
+        if (common_b[i].label == r.label) {
+          X.common.push_back(common_b[i]);
+          Y.common.push_back(common_a[i]);
+        }
+  }
+  p->rows_x = p->x_is_a ? m : n;
+  p->rows_y = p->x_is_a ? n : m;
+  for (Operand* op : {&X, &Y}) {
+    int64_t rows = 1;
+    for (auto& l : op->free) rows *= l.dim;
+    op->rows = rows;
+    op->in_place = matrix_view(op->free, op->common, &op->ld);
+    if (!op->in_place) {
+      build_gather(*op);
+      op->ld = k;
+    }
+  }
+  // output order
+  std::vector<Leg> def_out;  // default order free_A ++ free_B with contiguous strides
+  for (auto& l : free_a) def_out.push_back(l);
+  for (auto& l : free_b) def_out.push_back(l);
+  p->custom_out = false;
+  if (out_rank >= 0) {
+    if (out_rank != static_cast<int32_t>(def_out.size())) {
+      delete p;
+      TNC_RET(TNC_ERR_PERMUTATION, "output labels are not a permutation of the free legs");
+    }
+    std::vector<int> used(def_out.size(), 0);
+    for (int t = 0; t < out_rank; ++t) {
+      int found = -1;
+      for (size_t i = 0; i < def_out.size(); ++i)
+        if (def_out[i].label == out_labels[t] && !used[i]) found = static_cast<int>(i);
+      if (found < 0) {
+        delete p;
+        TNC_RET(TNC_ERR_PERMUTATION, "output labels are not a permutation of the free legs");
+      }
+      used[found] = 1;
+      p->out_perm.push_back(found);
+      if (found != t) p->custom_out = true;
+    }
+  }
+  p->out_rank = static_cast<int32_t>(def_out.size());
+  if (p->custom_out) {
+    for (int t = 0; t < p->out_rank; ++t) {
+      p->out_labels.push_back(def_out[p->out_perm[t]].label);
+      p->out_dims.push_back(def_out[p->out_perm[t]].dim);
+    }
+    int64_t s = 1;
+    std::vector<int64_t> st(def_out.size());
+    for (int i = static_cast<int>(def_out.size()) - 1; i >= 0; --i) {
+      st[i] = s;
+      s *= def_out[i].dim;
+    }
+    for (auto& l : def_out) p->out_perm_dims.push_back(l.dim);
+    p->out_perm_strides = st;
+  } else {
+    for (auto& l : def_out) {
+      p->out_labels.push_back(l.label);
+      p->out_dims.push_back(l.dim);
+    }
+  }
+  // default-order C strides for C[x_row, y_row]
+  if (p->x_is_a) {
+    p->ldcm = n;
+    p->ldcn = 1;
+  } else {
+    p->ldcm = 1;
+    p->ldcn = m;
+  }
+  // variant
+  int want = variant;
+  if (want == TNC_VARIANT_AUTO) want = tc_eligible(p) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_SIMT;
+  if (want == TNC_VARIANT_TC3XTF32 && p->dtype != TNC_C64) {
+    delete p;
+    TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
+  }
+  if (want == TNC_VARIANT_SPLITK) want = TNC_VARIANT_TC3XTF32;
+  p->variant = want;
+  p->kp = ((k + 15) / 16) * 16;
+  // split-K when the output tile grid cannot fill the machine
+  p->k_splits = 1;
+  if (p->variant == TNC_VARIANT_TC3XTF32) {
+    const int64_t bn = (2 * p->rows_y >= 256) ? 256 : 128;
+    const int64_t tiles = ceil_div(2 * p->rows_y, bn) * ceil_div(p->rows_x, 128);
+    const int64_t kblocks = 2 * p->kp / 32;
+    const int sms = num_sms();
+    if (tiles < sms && kblocks >= 8) {
+      int64_t want_splits = std::min<int64_t>(sms / tiles, kblocks / 4);
+      p->k_splits = static_cast<int32_t>(std::max<int64_t>(1, want_splits));
+    }
+  }
+  // workspace
+  const size_t eb = elem_bytes(p->dtype);
+  size_t off = 0;
+  p->off_x = off;
+  if (!X.in_place) off = align_up(off + static_cast<size_t>(p->rows_x) * k * eb);
+  p->off_y = off;
+  if (!Y.in_place) off = align_up(off + static_cast<size_t>(p->rows_y) * k * eb);
+  p->off_planes = off;
+  if (p->variant == TNC_VARIANT_TC3XTF32) {
+    const size_t a_plane = static_cast<size_t>(p->rows_x) * 2 * p->kp * 4;
+    const size_t b_plane = static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * 4;
+    off = align_up(off + 2 * a_plane + 2 * b_plane);
+  }
+  p->off_partials = off;
+  if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
+  p->off_tmp = off;
+  if (p->custom_out) off = align_up(off + static_cast<size_t>(m) * n * eb);
+  p->ws_bytes = off;
+  *plan_out = p;
+  return TNC_OK;
+}
+
+int tnc_plan_get_info(const tnc_plan* p, tnc_plan_info* info) {
+  if (!p || !info) TNC_RET(TNC_ERR_INVALID, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->m = p->m;
+  info->k = p->k;
+  info->n = p->n;
+  info->n_common = p->n_common;
+  info->variant = p->variant;
+  info->b_is_multiplier = p->b_is_multiplier;
+  info->out_rank = p->out_rank;
+  for (int i = 0; i < p->out_rank; ++i) {
+    info->out_labels[i] = p->out_labels[i];
+    info->out_dims[i] = p->out_dims[i];
+  }
+  info->workspace_bytes = p->ws_bytes;
+  info->multiplies_lo = p->multiplies > static_cast<__int128>(INT64_MAX)
+                            ? INT64_MAX
+                            : static_cast<int64_t>(p->multiplies);
+  return TNC_OK;
+}
+
+void tnc_plan_destroy(tnc_plan* p) { delete p; }
+
+static int prep_operand(const tnc_plan* p, const Operand& op, const void* src, uint8_t* ws,
+                        size_t off, const void** mat, int64_t* ld, cudaStream_t st) {
+  if (op.in_place) {
+    *mat = src;
+    *ld = op.ld;
+    return TNC_OK;
+  }
+  void* dst = ws + off;
+  TNC_TRY(permute_launch(p->dtype, static_cast<int>(op.dims.size()), op.dims.data(),
+                         op.strides.data(), op.perm.data(), src, dst, st));
+  *mat = dst;
+  *ld = p->k;
+  return TNC_OK;
+}
+
+static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* ym, int64_t ldy,
+                    void* c, int64_t ldcm, int64_t ldcn, uint8_t* ws, int k_splits,
+                    cudaStream_t st) {
+  if (p->variant == TNC_VARIANT_TC3XTF32) {
+    const size_t a_plane = static_cast<size_t>(p->rows_x) * 2 * p->kp * 4;
+    const size_t b_plane = static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * 4;
+    float* ab = reinterpret_cast<float*>(ws + p->off_planes);
+    float* as = reinterpret_cast<float*>(ws + p->off_planes + a_plane);
+    float* bb = reinterpret_cast<float*>(ws + p->off_planes + 2 * a_plane);
+    float* bs = reinterpret_cast<float*>(ws + p->off_planes + 2 * a_plane + b_plane);
+    TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
+    TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));
+    return tc_cgemm_launch(p->rows_x, p->rows_y, p->kp, ab, as, bb, bs, c, ldcm, ldcn, k_splits,
+                           reinterpret_cast<float*>(ws + p->off_partials), st);
+  }
+  return simt_cgemm_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ldx, ym, ldy, c, ldcm, ldcn,
+                           0, st);
+}
+
+int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void* workspace,
+                 size_t ws_bytes, void* stream) {
+  if (!p) TNC_RET(TNC_ERR_INVALID, "null plan");
+  if (ws_bytes < p->ws_bytes) TNC_RET(TNC_ERR_WORKSPACE, "workspace smaller than plan requires");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const void* xsrc = p->x_is_a ? a : b;
+  const void* ysrc = p->x_is_a ? b : a;
+  const void *xm, *ym;
+  int64_t ldx, ldy;
+  TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
+  TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
+  void* dst = p->custom_out ? static_cast<void*>(ws + p->off_tmp) : c;
+  TNC_TRY(run_gemm(p, xm, ldx, ym, ldy, dst, p->ldcm, p->ldcn, ws, p->k_splits, st));
+  if (p->custom_out) {
+    TNC_TRY(permute_launch(p->dtype, static_cast<int>(p->out_perm.size()),
+                           p->out_perm_dims.data(), p->out_perm_strides.data(),
+                           p->out_perm.data(), dst, c, st));
+  }
+  return TNC_OK;
+}
+
+int tnc_contract_split_workspace(const tnc_plan* p, int32_t blocks, int32_t group,
+                                 size_t* workspace_bytes) {
+  if (!p || !workspace_bytes) TNC_RET(TNC_ERR_INVALID, "null argument");
+  if (blocks < 1 || group < 1) TNC_RET(TNC_ERR_CONTRACTION, "blocks*group_size must be positive");
+  const int64_t panels = std::min<int64_t>(static_cast<int64_t>(blocks) * group, p->k);
+  const size_t eb = elem_bytes(p->dtype);
+  size_t need = align_up(p->ws_bytes) + align_up(static_cast<size_t>(panels) * p->m * p->n * eb);
+  // operand gathers are always materialised for the split path
+  need += align_up(static_cast<size_t>(p->rows_x) * p->k * eb) +
+          align_up(static_cast<size_t>(p->rows_y) * p->k * eb);
+  *workspace_bytes = need;
+  return TNC_OK;
+}
+
+int tnc_contract_split(const tnc_plan* p, int32_t blocks, int32_t group, const void* a,
+                       const void* b, void* c, void* workspace, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  TNC_TRY(tnc_contract_split_workspace(p, blocks, group, &need));
+  if (ws_bytes < need) TNC_RET(TNC_ERR_WORKSPACE, "workspace smaller than split plan requires");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int64_t panels = std::min<int64_t>(static_cast<int64_t>(blocks) * group, p->k);
+  const int64_t base = p->k / panels;
+  const size_t eb = elem_bytes(p->dtype);
+  uint8_t* parts = ws + align_up(p->ws_bytes);
+  const void* xsrc = p->x_is_a ? a : b;
+  const void* ysrc = p->x_is_a ? b : a;
+  const void *xm, *ym;
+  int64_t ldx, ldy;
+  TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
+  TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
+  const int64_t mn = p->m * p->n;
+  // each panel accumulates independently into its own [rows_x, rows_y] tile
+  for (int64_t i = 0; i < panels; ++i) {
+    const int64_t lo = i * base;
+    const int64_t hi = (i == panels - 1) ? p->k : lo + base;
+    const uint8_t* xp = static_cast<const uint8_t*>(xm) + static_cast<size_t>(lo) * eb;
+    const uint8_t* yp = static_cast<const uint8_t*>(ym) + static_cast<size_t>(lo) * eb;
+    void* dst = parts + static_cast<size_t>(i) * mn * eb;
+    TNC_TRY(simt_cgemm_launch(p->dtype, p->rows_x, p->rows_y, hi - lo, xp, ldx, yp, ldy, dst,
+                              p->rows_y, 1, 0, st));
+  }
+  // combine with the fixed pairwise tree, then place into the output layout
+  void* dst = p->custom_out ? static_cast<void*>(ws + p->off_tmp) : c;
+  TNC_TRY(tree_reduce_launch(p->dtype, panels, mn, parts, dst, p->rows_x, p->rows_y, p->ldcm,
+                             p->ldcn, st));
+  if (p->custom_out) {
+    TNC_TRY(permute_launch(p->dtype, static_cast<int>(p->out_perm.size()),
+                           p->out_perm_dims.data(), p->out_perm_strides.data(),
+                           p->out_perm.data(), dst, c, st));
+  }
+  return TNC_OK;
+}
+
+int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* axes,
+                               size_t* workspace_bytes) {
+  (void)axes;
+  (void)n_gates;
+  if (!workspace_bytes) TNC_RET(TNC_ERR_INVALID, "null argument");
+  if (t_rank < 2 || t_rank > 40) TNC_RET(TNC_ERR_TENSOR, "absorb: rank out of range");
+  *workspace_bytes = 0;
+  return TNC_OK;
+}
+
+int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,
+                     const void* const* gates, const int32_t* axes, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  return absorb_chain_launch(t_rank, t_in, t_out, n_gates, gates, axes, workspace,
+                             workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// Shared helpers of the B200 TNC kernels: status handling, complex types,
+// small device utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/tnc_b200.h"
+
+namespace tnc {
+
+// thread-local last error message (tnc_last_error)
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define TNC_RET(code, msg)               \
+  do {                                   \
+    ::tnc::set_error(msg);               \
+    return (code);                       \
+  } while (0)
+
+#define TNC_CUDA_TRY(expr)                                                       \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::tnc::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+      return TNC_ERR_CUDA;                                                       \
+    }                                                                            \
+  } while (0)
+
+#define TNC_CHECK_LAUNCH()                                                       \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::tnc::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return TNC_ERR_CUDA;                                                       \
+    }                                                                            \
+  } while (0)
+
+#define TNC_TRY(expr)          \
+  do {                         \
+    int _s = (expr);           \
+    if (_s != TNC_OK) return _s; \
+  } while (0)
+
+// complex element types (interleaved re, im), 8 and 16 bytes
+struct __align__(8) c64 {
+  float re, im;
+};
+struct __align__(16) c128 {
+  double re, im;
+};
+
+template <typename T> struct real_of;
+template <> struct real_of<c64> { using type = float; };
+template <> struct real_of<c128> { using type = double; };
+
+inline int num_sms() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+inline size_t elem_bytes(int dtype) { return dtype == TNC_C128 ? 16 : 8; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Compact description of a strided n-d view used by the gather kernels.
+struct Axis {
+  int64_t dim;
+  int64_t in_stride;
+  int64_t out_stride;
+};
+
+// ---- entry points implemented in the kernel translation units ----
+// permute: general strided -> contiguous (target order)
+int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
+                   const int32_t* perm, const void* in, void* out, cudaStream_t stream);
+// strided 2-d -> contiguous row-major gather, rows/cols each a group of legs
+// (used by the contraction prep).  Equivalent to permute with the given axes.
+// SIMT complex GEMM: C[m*ldcm + n*ldcn] = sum_k X[m*ldx + k] * Y[n*ldy + k]
+int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
+                      const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn,
+                      int accumulate, cudaStream_t stream);
+// axpy y += x
+int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream);
+// 3xTF32 prep: split complex X[R, K] (row-major, K contiguous, leading dim ldx)
+// into tf32 big / small planes.  mode 0: "A" planes (interleaved copy) of shape
+// [R, 2*Kp]; mode 1: "B" expanded planes of shape [2R, 2*Kp] (rows 2r: (re,-im),
+// 2r+1: (im, re)).  Columns >= 2K are zero.
+int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
+                      void* big, void* small, cudaStream_t stream);
+// tcgen05 3xTF32 complex GEMM on prepared planes (see tnc_gemm_tc.cu)
+int tc_cgemm_launch(int64_t M, int64_t N, int64_t Kp, const float* Abig, const float* Asmall,
+                    const float* Bbig, const float* Bsmall, void* C, int64_t ldcm, int64_t ldcn,
+                    int k_splits, float* partials, cudaStream_t stream);
+// fixed-order pairwise tree reduction of P partial [M,N] fp32-complex buffers
+int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out_or_null,
+                       int64_t M, int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream);
+
+// K4 step fusion (tnc_absorb.cu)
+int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates,
+                        const void* const* gates, const int32_t* axes, void* workspace,
+                        size_t workspace_bytes, cudaStream_t stream);
+
+}  // namespace tnc

@@ -1,0 +1,337 @@
+// CUDA-core complex GEMM for small / awkward contraction steps, plus the
+// element-wise helpers (axpy, 3xTF32 plane split, fixed-order tree reduce).
+//
+// Reference op: the np.matmul of contract_pair (contract.py:131-165).  Used
+// where a step is too small to feed tensor cores (most of the ~800 steps of
+// a circuit slice) or for complex128 ("double" precision) tensors.
+#include <algorithm>
+
+#include "tnc_common.cuh"
+
+namespace tnc {
+
+namespace {
+
+template <typename R>
+struct cpx {
+  R re, im;
+};
+
+template <typename T>
+__device__ __forceinline__ cpx<typename real_of<T>::type> load_c(const T* p) {
+  T v = *p;
+  return {v.re, v.im};
+}
+
+// C[m*ldcm + n*ldcn] (+)= sum_k X[m*ldx + k] * Y[n*ldy + k]
+// 64x64 output tile per 256-thread block, 4x4 complex outputs per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) simt_cgemm_kernel(int64_t M, int64_t N, int64_t K,
+                                                         const T* __restrict__ X, int64_t ldx,
+                                                         const T* __restrict__ Y, int64_t ldy,
+                                                         T* __restrict__ C, int64_t ldcm,
+                                                         int64_t ldcn, int accumulate) {
+  using R = typename real_of<T>::type;
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ R xs_re[BK][BM + 1], xs_im[BK][BM + 1];
+  __shared__ R ys_re[BK][BN + 1], ys_im[BK][BN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  R acc_re[4][4], acc_im[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc_re[i][j] = acc_im[i][j] = R(0);
+
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    // each thread loads 4 elements of X and 4 of Y (k fastest for coalescing)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int idx = tid + r * 256;  // 0..1023
+      int kk = idx & (BK - 1);
+      int mm = idx >> 4;
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      R vr = R(0), vi = R(0);
+      if (gm < M && gk < K) {
+        T v = X[gm * ldx + gk];
+        vr = v.re;
+        vi = v.im;
+      }
+      xs_re[kk][mm] = vr;
+      xs_im[kk][mm] = vi;
+      int64_t gn = n0 + mm;
+      vr = R(0);
+      vi = R(0);
+      if (gn < N && gk < K) {
+        T v = Y[gn * ldy + gk];
+        vr = v.re;
+        vi = v.im;
+      }
+      ys_re[kk][mm] = vr;
+      ys_im[kk][mm] = vi;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      R ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ar[i] = xs_re[kk][ty + 16 * i];
+        ai[i] = xs_im[kk][ty + 16 * i];
+        br[i] = ys_re[kk][tx + 16 * i];
+        bi[i] = ys_im[kk][tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc_re[i][j] = fma(ar[i], br[j], acc_re[i][j]);
+          acc_re[i][j] = fma(-ai[i], bi[j], acc_re[i][j]);
+          acc_im[i][j] = fma(ar[i], bi[j], acc_im[i][j]);
+          acc_im[i][j] = fma(ai[i], br[j], acc_im[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t gn = n0 + tx + 16 * j;
+      if (gn >= N) continue;
+      T* p = C + gm * ldcm + gn * ldcn;
+      T v;
+      v.re = acc_re[i][j];
+      v.im = acc_im[i][j];
+      if (accumulate) {
+        T o = *p;
+        v.re += o.re;
+        v.im += o.im;
+      }
+      *p = v;
+    }
+  }
+}
+
+// Tiny-K / tiny-N path: one thread per output element, full K loop.
+template <typename T>
+__global__ void __launch_bounds__(256) simt_dot_kernel(int64_t M, int64_t N, int64_t K,
+                                                       const T* __restrict__ X, int64_t ldx,
+                                                       const T* __restrict__ Y, int64_t ldy,
+                                                       T* __restrict__ C, int64_t ldcm,
+                                                       int64_t ldcn, int accumulate) {
+  using R = typename real_of<T>::type;
+  const int64_t total = M * N;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t m, n;
+    if (ldcn == 1) {  // walk the output contiguously
+      m = e / N;
+      n = e - m * N;
+    } else {
+      n = e / M;
+      m = e - n * M;
+    }
+    const T* xr = X + m * ldx;
+    const T* yr = Y + n * ldy;
+    R re = R(0), im = R(0);
+    for (int64_t k = 0; k < K; ++k) {
+      T a = xr[k], b = yr[k];
+      re = fma(a.re, b.re, re);
+      re = fma(-a.im, b.im, re);
+      im = fma(a.re, b.im, im);
+      im = fma(a.im, b.re, im);
+    }
+    T* p = C + m * ldcm + n * ldcn;
+    if (accumulate) {
+      T o = *p;
+      re += o.re;
+      im += o.im;
+    }
+    T v;
+    v.re = re;
+    v.im = im;
+    *p = v;
+  }
+}
+
+template <typename T>
+__global__ void axpy_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ y) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    T a = x[i], b = y[i];
+    b.re += a.re;
+    b.im += a.im;
+    y[i] = b;
+  }
+}
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// 3xTF32 operand planes.  mode 0: big/small of the interleaved row [2*Kp];
+// mode 1: expanded rows 2r = (re, -im), 2r+1 = (im, re) per complex k.
+__global__ void tf32_split_kernel(int mode, int64_t R, int64_t K, int64_t Kp,
+                                  const c64* __restrict__ X, int64_t ldx, float* __restrict__ big,
+                                  float* __restrict__ small) {
+  const int64_t total = R * Kp;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = e / Kp;
+    int64_t k = e - r * Kp;
+    float re = 0.f, im = 0.f;
+    if (k < K) {
+      c64 v = X[r * ldx + k];
+      re = v.re;
+      im = v.im;
+    }
+    float bre = tf32_round(re), bim = tf32_round(im);
+    float sre = re - bre, sim = im - bim;
+    if (mode == 0) {
+      float2* b2 = reinterpret_cast<float2*>(big) + r * Kp + k;
+      float2* s2 = reinterpret_cast<float2*>(small) + r * Kp + k;
+      *b2 = make_float2(bre, bim);
+      *s2 = make_float2(sre, sim);
+    } else {
+      float2* b0 = reinterpret_cast<float2*>(big) + (2 * r) * Kp + k;
+      float2* s0 = reinterpret_cast<float2*>(small) + (2 * r) * Kp + k;
+      float2* b1 = b0 + Kp;
+      float2* s1 = s0 + Kp;
+      *b0 = make_float2(bre, -bim);
+      *s0 = make_float2(sre, -sim);
+      *b1 = make_float2(bim, bre);
+      *s1 = make_float2(sim, sre);
+    }
+  }
+}
+
+// Fixed-order pairwise tree over P partial tiles [P][MN] (complex, fp32 or
+// fp64): level by level, partial i += partial i+stride, exactly the
+// left-complete combine of contract.py:200-207.  The root is written to
+// out (strided) if given.
+template <typename T>
+__global__ void tree_level_kernel(int64_t P, int64_t MN, int64_t stride, T* __restrict__ parts) {
+  // pairs (i, i+stride) for i multiple of 2*stride
+  const int64_t n_pairs = (P + 2 * stride - 1) / (2 * stride);
+  const int64_t total = n_pairs * MN;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t pair = e / MN;
+    int64_t off = e - pair * MN;
+    int64_t i = pair * 2 * stride;
+    int64_t j = i + stride;
+    if (j >= P) continue;
+    T a = parts[i * MN + off], b = parts[j * MN + off];
+    a.re += b.re;
+    a.im += b.im;
+    parts[i * MN + off] = a;
+  }
+}
+
+template <typename T>
+__global__ void scatter_mn_kernel(int64_t M, int64_t N, const T* __restrict__ src,
+                                  T* __restrict__ dst, int64_t ldcm, int64_t ldcn) {
+  const int64_t total = M * N;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t m = e / N, n = e - (e / N) * N;
+    dst[m * ldcm + n * ldcn] = src[e];
+  }
+}
+
+inline unsigned grid_for(int64_t work, int threads = 256) {
+  int64_t blocks = ceil_div(work, threads);
+  blocks = std::min<int64_t>(blocks, static_cast<int64_t>(num_sms()) * 32);
+  return static_cast<unsigned>(std::max<int64_t>(blocks, 1));
+}
+
+}  // namespace
+
+int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
+                      const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn,
+                      int accumulate, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return TNC_OK;
+  const bool tiled = (M >= 32 && N >= 32 && K >= 8);
+  if (tiled) {
+    dim3 grid(static_cast<unsigned>(ceil_div(N, 64)), static_cast<unsigned>(ceil_div(M, 64)));
+    if (grid.y > 65535) {
+      // fall back to the dot kernel for enormous M (grid.y limit)
+    } else {
+      if (dtype == TNC_C128)
+        simt_cgemm_kernel<c128><<<grid, 256, 0, stream>>>(
+            M, N, K, static_cast<const c128*>(X), ldx, static_cast<const c128*>(Y), ldy,
+            static_cast<c128*>(C), ldcm, ldcn, accumulate);
+      else
+        simt_cgemm_kernel<c64><<<grid, 256, 0, stream>>>(
+            M, N, K, static_cast<const c64*>(X), ldx, static_cast<const c64*>(Y), ldy,
+            static_cast<c64*>(C), ldcm, ldcn, accumulate);
+      TNC_CHECK_LAUNCH();
+      return TNC_OK;
+    }
+  }
+  unsigned g = grid_for(M * N);
+  if (dtype == TNC_C128)
+    simt_dot_kernel<c128><<<g, 256, 0, stream>>>(M, N, K, static_cast<const c128*>(X), ldx,
+                                                  static_cast<const c128*>(Y), ldy,
+                                                  static_cast<c128*>(C), ldcm, ldcn, accumulate);
+  else
+    simt_dot_kernel<c64><<<g, 256, 0, stream>>>(M, N, K, static_cast<const c64*>(X), ldx,
+                                                static_cast<const c64*>(Y), ldy,
+                                                static_cast<c64*>(C), ldcm, ldcn, accumulate);
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream) {
+  if (n <= 0) return TNC_OK;
+  unsigned g = grid_for(n);
+  if (dtype == TNC_C128)
+    axpy_kernel<c128><<<g, 256, 0, stream>>>(n, static_cast<const c128*>(x), static_cast<c128*>(y));
+  else
+    axpy_kernel<c64><<<g, 256, 0, stream>>>(n, static_cast<const c64*>(x), static_cast<c64*>(y));
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
+                      void* big, void* small, cudaStream_t stream) {
+  if (R <= 0 || Kp <= 0) return TNC_OK;
+  tf32_split_kernel<<<grid_for(R * Kp), 256, 0, stream>>>(
+      mode, R, K, Kp, static_cast<const c64*>(X), ldx, static_cast<float*>(big),
+      static_cast<float*>(small));
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out, int64_t M,
+                       int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream) {
+  for (int64_t stride = 1; stride < P; stride *= 2) {
+    int64_t pairs = (P + 2 * stride - 1) / (2 * stride);
+    unsigned g = grid_for(pairs * MN);
+    if (dtype == TNC_C128)
+      tree_level_kernel<c128><<<g, 256, 0, stream>>>(P, MN, stride, static_cast<c128*>(partials));
+    else
+      tree_level_kernel<c64><<<g, 256, 0, stream>>>(P, MN, stride, static_cast<c64*>(partials));
+    TNC_CHECK_LAUNCH();
+  }
+  if (out) {
+    unsigned g = grid_for(M * N);
+    if (dtype == TNC_C128)
+      scatter_mn_kernel<c128><<<g, 256, 0, stream>>>(M, N, static_cast<const c128*>(partials),
+                                                     static_cast<c128*>(out), ldcm, ldcn);
+    else
+      scatter_mn_kernel<c64><<<g, 256, 0, stream>>>(M, N, static_cast<const c64*>(partials),
+                                                    static_cast<c64*>(out), ldcm, ldcn);
+    TNC_CHECK_LAUNCH();
+  }
+  return TNC_OK;
+}
+
+}  // namespace tnc
