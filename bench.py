@@ -1,0 +1,361 @@
+"""Benchmark of the B200 TNC hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3|c1a|c1b|c1c] [--slices-per-step S]
+
+Default workload (config C3 of BASELINE.json, the largest single-GPU one the
+metric "TNC effective TFLOP/s & slices/s" is quoted on): 6x6 grid random
+circuit, 14 cycles, seed 0, 64 correlated amplitudes (qubits 30-35 open),
+reference greedy path (seed 0), reference slicing to rank <= 30 (9 labels,
+512 slices).  One *step* = S slices per GPU (weak scaling: slice ids are
+dealt round-robin over ranks), each slice contracted with slice-invariant
+reuse; partial amplitudes accumulate on device and are summed with one NCCL
+all-reduce.  value = effective TFLOP/s (8 * sum M*K*N, the reference's cost
+convention) over all ranks; slices/s is reported beside it.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy oracle port of tncsim's permute+matmul step loop, all host threads) on a
+bounded sub-slice sample of the same workload, same metric/unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TNC effective TFLOP/s & slices/s at 1/2/4/8 B200; % of roofline per step"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() in ("active", "1"):
+                    reasons.add(name)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measure_tf32_peak() -> dict:
+    """cuBLAS TF32 GEMM throughput on this GPU (MEASURED_PEAKS.json has no
+    TF32 entry): fp32 8192^3 matmul with TF32 enabled, best of 10 (burst)."""
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = True
+    n = 8192
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    for _ in range(3):
+        a @ b
+    best = float("inf")
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return {"tf32_tflops": 2 * n ** 3 / best / 1e12, "how": "torch fp32 matmul 8192^3, allow_tf32, best of 10"}
+
+
+def measured_peaks() -> dict:
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        return json.loads(path.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+# -- workload C3 ---------------------------------------------------------------
+
+
+def plan_c3():
+    from paper_2504_09186_b200 import greedy_path, linearize, select_slices, tree_metrics
+    from paper_2504_09186_b200 import workloads
+
+    wl = workloads.C3
+    net = wl.network()
+    t = greedy_path(net, 0)
+    spec = select_slices(t, workloads.C3_MAX_RANK, 64, 0)
+    s = linearize(t)
+    per_slice = tree_metrics(t, spec.dims_projected()).total_cost
+    return wl, net, t, s, spec, per_slice
+
+
+def _oracle_leaves(net):
+    from oracle import tncref
+
+    return tncref.cast_leaves([(t.labels, t.dims, t.numpy()) for t in net.tensors], "single")
+
+
+def run_cpu_subslice(net, s, sub, sid: int = 0) -> float:
+    from oracle import tncref
+
+    leaves = _oracle_leaves(net)
+    steps = [(st.lhs, st.rhs, st.result) for st in s.steps]
+    t0 = time.perf_counter()
+    tncref.run_range(leaves, steps, s.n_leaves, 1, len(steps), sub.assignment(sid), {}, "single")
+    return time.perf_counter() - t0
+
+
+def _threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def bench_reference(args) -> None:
+    """--impl reference: the reference algorithm on the host cores."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(_threads()))
+    from paper_2504_09186_b200 import tree_metrics
+
+    wl, net, t, s, spec, per_slice = plan_c3()
+    from paper_2504_09186_b200 import select_slices
+
+    sub = select_slices(t, args.ref_cap, 64, 0)
+    mult = tree_metrics(t, sub.dims_projected()).total_cost
+    for i in range(args.warmup):
+        run_cpu_subslice(net, s, sub, i)
+    times = [run_cpu_subslice(net, s, sub, args.warmup + i) for i in range(args.steps)]
+    total = sum(times)
+    value = 8 * mult * args.steps / total / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded grid RQC)",
+        "config": {"workload": f"C3 6x6x14 seed 0, 64 open amps; each step = one sub-slice (cap {args.ref_cap}, "
+                               f"{len(sub.entries)} sliced labels) of the cap-30 slicing",
+                   "slices_per_s_extrapolated": (args.steps / total) * mult / per_slice},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": _threads(), "kind": "port",
+                         "sample": f"{args.steps} C3 sub-slices at cap {args.ref_cap} ({mult} multiplies each), "
+                                   "numpy oracle of tncsim permute+matmul (complex128 in flight)"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_c3(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_09186_b200 import _lib
+    from paper_2504_09186_b200.execute import SliceExecutor, run_open
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load(require_device=True)
+    wl, net, t, s, spec, per_slice = plan_c3()
+    order = wl.output_order()
+    ex = SliceExecutor(net, s, spec, "single", order)
+    ex.prepare()
+    n_slices = spec.n_subtasks
+    spp = args.slices_per_step
+
+    def ids_for(step: int):
+        base = (step * world + rank) * spp
+        return [(base + j) % n_slices for j in range(spp)]
+
+    acc = None
+    for i in range(args.warmup):
+        acc = ex.run(ids_for(i), acc)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    lib.tnc_profile_enable(1)
+    launches0 = lib.tnc_launch_count()
+    stream = torch.cuda.current_stream()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    part = None
+    for i in range(args.steps):
+        part = ex.run(ids_for(args.warmup + i), part)
+    if world > 1:
+        dist.all_reduce(part.data.view(torch.float32), op=dist.ReduceOp.SUM)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.tnc_launch_count() - launches0
+    elapsed = start.elapsed_time(stop) / 1e3
+    if world > 1:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = tt.item()
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    prof = _read_prof(lib)
+    lib.tnc_profile_enable(0)
+    slices_total = args.steps * spp * world
+    flops_total = 8 * per_slice * slices_total
+    value = flops_total / elapsed / 1e12
+
+    # end to end through the public API: host-resident leaves (pinned) uploaded
+    # every step, slice contracted, amplitudes read back to the host.
+    e2e = None
+    if rank == 0 and args.e2e_steps > 0:
+        host_leaves = [tt_.data.detach().cpu().pin_memory() for tt_ in net.tensors]
+        h2d = sum(x.numel() * x.element_size() for x in host_leaves)
+        from paper_2504_09186_b200 import DenseTensor, TensorNetwork
+
+        torch.cuda.synchronize()
+        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_s.record()
+        d2h = 0
+        for i in range(args.e2e_steps):
+            dev = [DenseTensor.__new__(DenseTensor)._init_raw(tt_.indices, hl.to("cuda", non_blocking=True))
+                   for tt_, hl in zip(net.tensors, host_leaves)]
+            amps = run_open(TensorNetwork(dev), t, spec, order, "single", slice_ids=[i]).data.cpu()
+            d2h = amps.numel() * amps.element_size()
+        e_e.record()
+        torch.cuda.synchronize()
+        e_t = e_s.elapsed_time(e_e) / 1e3
+        e2e = {"value": 8 * per_slice * args.e2e_steps / e_t / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "slices_per_s": args.e2e_steps / e_t}
+
+    if rank == 0:
+        peaks = measured_peaks()
+        tf32 = measure_tf32_peak()
+        p_eff = tf32["tf32_tflops"] / 3.0
+        tc = prof["tc_gemm"]
+        achieved = tc["flops"] / (tc["ms"] / 1e3) / 1e12 if tc["ms"] > 0 else None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from paper_2504_09186_b200 import select_slices, tree_metrics
+
+            os.environ.setdefault("OPENBLAS_NUM_THREADS", str(_threads()))
+            sub = select_slices(t, args.cpu_cap, 64, 0)
+            mult = tree_metrics(t, sub.dims_projected()).total_cost
+            secs = run_cpu_subslice(net, s, sub, 0)
+            cpu = {"value": 8 * mult / secs / 1e12, "unit": "TFLOP/s", "cores": _threads(), "kind": "port",
+                   "sample": f"one C3 sub-slice (extra slicing to rank {args.cpu_cap}: {len(sub.entries)} labels, "
+                             f"{mult} multiplies) through the numpy oracle of tncsim's step loop, {secs:.1f}s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (3xTF32 tensor-core GEMM, fp32 accumulate)",
+            "data": "synthetic (seeded 6x6 grid random circuit, SURVEY Appendix A)",
+            "config": {"workload": "C3: 6x6 grid, 14 cycles, seed 0, 64 open amplitudes (q30-35), greedy path "
+                                   "seed 0, slices to rank<=30 (9 labels, 512 slices)",
+                       "slices_per_step_per_gpu": spp, "slices_per_s": slices_total / elapsed,
+                       "flops_per_slice": 8 * per_slice, "l2": "inputs > L2 (intermediates up to 8 GiB)",
+                       "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_eff, "unit": "TFLOP/s",
+                         "frac": (achieved / p_eff) if achieved else None, "traffic": None,
+                         "kernel": "tc_cgemm_kernel (3xTF32 tcgen05)",
+                         "peak_source": f"measured cuBLAS TF32 {tf32['tf32_tflops']:.0f} TF/s / 3 (3xTF32); "
+                                        "MEASURED_PEAKS.json has no TF32 entry",
+                         "launches": tc["launches"], "share_of_step": tc["ms"] / 1e3 / elapsed},
+            "kernels": prof, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+            "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "tf32_tflops": tf32["tf32_tflops"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _read_prof(lib) -> dict:
+    import ctypes
+
+    out = {}
+    for kind, name in enumerate(["tc_gemm", "simt_gemm", "permute", "split_prep", "reduce", "absorb", "axpy"]):
+        n = ctypes.c_int64()
+        ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        lib.tnc_profile_read(kind, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by))
+        out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c3"])
+    ap.add_argument("--slices-per-step", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-cap", type=int, default=26)
+    ap.add_argument("--ref-cap", type=int, default=25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    import paper_2504_09186_b200._lib as _l  # noqa: F401  (fail fast if the package is broken)
+    if args.impl == "reference":
+        bench_reference(args)
+        return
+    bench_c3(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,18 @@ int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* a
 /* y[i] += x[i] for n complex elements. */
 int tnc_axpy(int32_t dtype, int64_t n, const void* x, void* y, void* stream);
 
+/* ---- measurement hooks (bench.py) ------------------------------------------
+ * tnc_launch_count: kernels this library has launched since load.
+ * tnc_profile_enable(1) clears and starts per-kernel CUDA-event timing on the
+ * launching stream; tnc_profile_read sums launches / device ms / algorithmic
+ * flops / algorithmic bytes for one kernel kind:
+ *   0 tensor-core GEMM, 1 CUDA-core GEMM, 2 permute, 3 3xTF32 operand prep,
+ *   4 split-K reduce, 5 absorb chain, 6 axpy. */
+int64_t tnc_launch_count(void);
+int tnc_profile_enable(int on);
+int tnc_profile_read(int32_t kind, int64_t* launches, double* total_ms, double* flops,
+                     double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -307,7 +307,7 @@ def section_sliced():
     import itertools
 
     per_slice = []
-    for key in itertools.product(*[range(d) for d in ospec.dims_projected().values()]):
+    for key in itertools.product(*[range(e.index.dim) for e in ospec.entries]):
         values = {}
         eng.run_range(os_, 1, len(os_.steps), dict(zip(ospec.labels, key)), values, RunStats())
         root = values[os_.steps[-1].result]

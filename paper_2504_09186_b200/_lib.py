@@ -72,6 +72,10 @@ SIGNATURES = {
                                         _P, _SZ, _P]),
     "tnc_absorb_chain_workspace": (ctypes.c_int, [_I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_SZ)]),
     "tnc_axpy": (ctypes.c_int, [_I32, _I64, _P, _P, _P]),
+    "tnc_launch_count": (ctypes.c_int64, []),
+    "tnc_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tnc_profile_read": (ctypes.c_int, [_I32, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None

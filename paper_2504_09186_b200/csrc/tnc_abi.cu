@@ -11,7 +11,10 @@
 //   * the GEMM epilogue writes C straight into the output layout
 //     (free_A ++ free_B, row- or column-oriented), no trailing transpose.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -23,6 +26,43 @@ namespace tnc {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
+
+// ---- launch counter and optional per-kernel event timing ----
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec {
+  int kind;
+  double flops, bytes;
+  cudaEvent_t start, stop;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::atomic<bool> g_prof_on{false};
+}  // namespace
+
+ProfScope::ProfScope(int kind, double flops, double bytes, cudaStream_t stream)
+    : kind_(kind), flops_(flops), bytes_(bytes), stream_(stream) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  if (cudaEventCreate(&start_) != cudaSuccess) {
+    start_ = nullptr;
+    return;
+  }
+  cudaEventRecord(start_, stream_);
+}
+
+ProfScope::~ProfScope() {
+  if (!start_) return;
+  cudaEvent_t stop = nullptr;
+  if (cudaEventCreate(&stop) != cudaSuccess) {
+    cudaEventDestroy(start_);
+    return;
+  }
+  cudaEventRecord(stop, stream_);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back({kind_, flops_, bytes_, start_, stop});
+}
 
 namespace {
 
@@ -153,6 +193,41 @@ using namespace tnc;
 extern "C" {
 
 int tnc_abi_version(void) { return TNC_ABI_VERSION; }
+
+int64_t tnc_launch_count(void) { return g_launches.load(); }
+
+int tnc_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.start);
+    cudaEventDestroy(r.stop);
+  }
+  g_prof.clear();
+  g_prof_on.store(on != 0);
+  return TNC_OK;
+}
+
+int tnc_profile_read(int32_t kind, int64_t* launches, double* total_ms, double* flops,
+                     double* bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int64_t n = 0;
+  double ms = 0, fl = 0, by = 0;
+  for (auto& r : g_prof) {
+    if (r.kind != kind) continue;
+    TNC_CUDA_TRY(cudaEventSynchronize(r.stop));
+    float t = 0.f;
+    TNC_CUDA_TRY(cudaEventElapsedTime(&t, r.start, r.stop));
+    ++n;
+    ms += t;
+    fl += r.flops;
+    by += r.bytes;
+  }
+  if (launches) *launches = n;
+  if (total_ms) *total_ms = ms;
+  if (flops) *flops = fl;
+  if (bytes) *bytes = by;
+  return TNC_OK;
+}
 
 const char* tnc_last_error(void) { return tnc::last_error(); }
 
@@ -313,8 +388,8 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     p->ldcm = n;
     p->ldcn = 1;
   } else {
-    p->ldcm = 1;
-    p->ldcn = m;
+    p->ldcm = 1;  // x enumerates free_B (fastest in free_A ++ free_B)
+    p->ldcn = n;
   }
   // variant
   int want = variant;
@@ -336,6 +411,10 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     if (tiles < sms && kblocks >= 8) {
       int64_t want_splits = std::min<int64_t>(sms / tiles, kblocks / 4);
       p->k_splits = static_cast<int32_t>(std::max<int64_t>(1, want_splits));
+    }
+    if (const char* env = std::getenv("TNC_KSPLIT")) {  // experiment override
+      const int64_t forced = std::atoll(env);
+      if (forced >= 1) p->k_splits = static_cast<int32_t>(std::min<int64_t>(forced, kblocks));
     }
   }
   // workspace
@@ -410,7 +489,7 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     float* bs = reinterpret_cast<float*>(ws + p->off_planes + 2 * a_plane + b_plane);
     TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
     TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));
-    return tc_cgemm_launch(p->rows_x, p->rows_y, p->kp, ab, as, bb, bs, c, ldcm, ldcn, k_splits,
+    return tc_cgemm_launch(p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs, c, ldcm, ldcn, k_splits,
                            reinterpret_cast<float*>(ws + p->off_partials), st);
   }
   return simt_cgemm_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ldx, ym, ldy, c, ldcm, ldcn,

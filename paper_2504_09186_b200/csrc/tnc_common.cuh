@@ -30,8 +30,13 @@ const char* last_error();
     }                                                                            \
   } while (0)
 
+// every kernel launch site ends with TNC_CHECK_LAUNCH(): it also counts the
+// launch (tnc_launch_count) so benchmarks can report how many of OUR kernels ran
+void count_launch();
+
 #define TNC_CHECK_LAUNCH()                                                       \
   do {                                                                           \
+    ::tnc::count_launch();                                                       \
     cudaError_t _e = cudaGetLastError();                                         \
     if (_e != cudaSuccess) {                                                     \
       ::tnc::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
@@ -79,6 +84,24 @@ struct Axis {
   int64_t out_stride;
 };
 
+// ---- optional per-kernel device timing (tnc_profile_*) ----
+enum ProfKind { PROF_TC_GEMM = 0, PROF_SIMT_GEMM = 1, PROF_PERMUTE = 2, PROF_SPLIT_PREP = 3,
+                PROF_REDUCE = 4, PROF_ABSORB = 5, PROF_AXPY = 6, PROF_KINDS = 7 };
+// RAII: when profiling is enabled, records CUDA events around the launches
+// issued in its scope on `stream` and books `flops` / `bytes` of algorithmic
+// work to `kind`.
+class ProfScope {
+ public:
+  ProfScope(int kind, double flops, double bytes, cudaStream_t stream);
+  ~ProfScope();
+
+ private:
+  int kind_;
+  double flops_, bytes_;
+  cudaStream_t stream_;
+  cudaEvent_t start_ = nullptr;
+};
+
 // ---- entry points implemented in the kernel translation units ----
 // permute: general strided -> contiguous (target order)
 int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
@@ -98,7 +121,7 @@ int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t strea
 int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
                       void* big, void* small, cudaStream_t stream);
 // tcgen05 3xTF32 complex GEMM on prepared planes (see tnc_gemm_tc.cu)
-int tc_cgemm_launch(int64_t M, int64_t N, int64_t Kp, const float* Abig, const float* Asmall,
+int tc_cgemm_launch(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Abig, const float* Asmall,
                     const float* Bbig, const float* Bsmall, void* C, int64_t ldcm, int64_t ldcn,
                     int k_splits, float* partials, cudaStream_t stream);
 // fixed-order pairwise tree reduction of P partial [M,N] fp32-complex buffers

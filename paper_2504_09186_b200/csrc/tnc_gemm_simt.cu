@@ -170,10 +170,14 @@ __global__ void axpy_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ 
   }
 }
 
+// Round to the nearest TF32 (ties away from zero) with the 13 low mantissa
+// bits explicitly zeroed, so `big` is exact in TF32 and x - big is exact in
+// fp32 (|small| <= 2^-12 |x|).
 __device__ __forceinline__ float tf32_round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;  // inf / nan unchanged
+  u = (u + 0x1000u) & 0xffffe000u;
+  return __uint_as_float(u);
 }
 
 // 3xTF32 operand planes.  mode 0: big/small of the interleaved row [2*Kp];
@@ -258,6 +262,8 @@ int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X,
                       const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn,
                       int accumulate, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return TNC_OK;
+  const double eb = static_cast<double>(elem_bytes(dtype));
+  ProfScope prof(PROF_SIMT_GEMM, 8.0 * M * N * K, eb * (double(M) * K + double(N) * K + double(M) * N), stream);
   const bool tiled = (M >= 32 && N >= 32 && K >= 8);
   if (tiled) {
     dim3 grid(static_cast<unsigned>(ceil_div(N, 64)), static_cast<unsigned>(ceil_div(M, 64)));
@@ -291,6 +297,7 @@ int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X,
 
 int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream) {
   if (n <= 0) return TNC_OK;
+  ProfScope prof(PROF_AXPY, 2.0 * n, 3.0 * n * elem_bytes(dtype), stream);
   unsigned g = grid_for(n);
   if (dtype == TNC_C128)
     axpy_kernel<c128><<<g, 256, 0, stream>>>(n, static_cast<const c128*>(x), static_cast<c128*>(y));
@@ -303,6 +310,7 @@ int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t strea
 int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
                       void* big, void* small, cudaStream_t stream) {
   if (R <= 0 || Kp <= 0) return TNC_OK;
+  ProfScope prof(PROF_SPLIT_PREP, 0.0, 8.0 * R * K + (mode ? 32.0 : 16.0) * R * Kp, stream);
   tf32_split_kernel<<<grid_for(R * Kp), 256, 0, stream>>>(
       mode, R, K, Kp, static_cast<const c64*>(X), ldx, static_cast<float*>(big),
       static_cast<float*>(small));
@@ -312,6 +320,7 @@ int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X,
 
 int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out, int64_t M,
                        int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream) {
+  ProfScope prof(PROF_REDUCE, 2.0 * P * MN, 2.0 * P * MN * elem_bytes(dtype), stream);
   for (int64_t stride = 1; stride < P; stride *= 2) {
     int64_t pairs = (P + 2 * stride - 1) / (2 * stride);
     unsigned g = grid_for(pairs * MN);

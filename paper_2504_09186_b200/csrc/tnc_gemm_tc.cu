@@ -4,19 +4,31 @@
 // which the reference runs in complex128 for "single" tensors
 // (execute.py:154-158).  fp32 accuracy is kept with the 3xTF32 scheme
 //     x*y ~= big(x)*big(y) + big(x)*small(y) + small(x)*big(y)
-// (big = rna-rounded TF32, small = x - big), all three products issued as
+// (big = nearest TF32, small = x - big), all three products issued as
 // tcgen05.mma kind::tf32 into one fp32 TMEM accumulator.
 //
 // Complex arithmetic is folded into ONE real GEMM:
 //     A  (complex [M, K], interleaved)      == real [M, 2K]
 //     B^ (real [2N, 2K], K-major): row 2n = (Br, -Bi) pairs, row 2n+1 = (Bi, Br)
 //     D = A . B^T  (real [M, 2N]) == complex C [M, N] interleaved.
-// The operand planes (big/small, zero-padded to Kp) are produced by
-// tf32_split_kernel; this kernel streams them with TMA (128B swizzle) into a
+// The operand planes (big/small, zero-padded to Kp) come from
+// tf32_split_kernel; this kernel streams them with TMA (swizzled) into a
 // multi-stage smem ring and one elected thread issues the MMAs.
 //
-// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
-// issuer, warps 2..5 = epilogue (TMEM -> registers -> global, any strides).
+// Accuracy: measured on B200, the tensor-core fp32 accumulation error grows
+// LINEARLY with the accumulation chain (rel-L2 ~1.4e-8 per complex K), so a
+// K = 2^15 contraction accumulated in TMEM alone would miss the 1e-5 contract.
+// The MMA warp therefore accumulates short K-chunks (kb_per_chunk k-blocks)
+// into alternating TMEM buffers and the epilogue warps fold each finished
+// chunk into fp32 registers with round-to-nearest adds (chain-length error
+// ~4e-7 per GEMM independent of K).
+//
+// Roles (320 threads, persistent over (split, m, n) work units):
+//   warp 0     TMA producer (one elected lane)
+//   warp 1     TMEM owner + MMA issuer (one elected lane)
+//   warps 2..9 chunk reducers / epilogue: warp w reads TMEM lane quadrant
+//              w % 4 and column half (w - 2) / 4, keeps BN/2 fp32 running sums
+//              per thread, writes C (any strides) or split-K partials.
 #include <cuda.h>
 
 #include <algorithm>
@@ -28,9 +40,9 @@ namespace tnc {
 
 namespace {
 
-constexpr int kBM = 128;        // rows of A per CTA (TMEM lanes)
-constexpr int kBK = 32;         // real K per stage = 128 B rows (SWIZZLE_128B atom)
-constexpr int kThreads = 192;
+constexpr int kBM = 128;  // rows of A per CTA (TMEM lanes)
+constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -46,17 +58,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(addr),
-      "r"(parity), "r"(0x989680)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x989680)
       : "memory");
+  return ok != 0;
+}
+
+// Bounded wait: a pipeline bug traps (context error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t spin = 0; !mbar_try(addr, parity); ++spin) {
+    if (spin > (1u << 24)) __trap();
+  }
 }
 
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
@@ -68,14 +93,16 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
-// K-major operand, 128B swizzle: 8-row atoms of 1024 B, SBO = 1024 B.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// K-major operand in the canonical swizzled layout: 8-row atoms of 8*SWZ
+// bytes (SBO), rows SWZ bytes long.  SWZ = 128 -> layout 2, SWZ = 64 -> 4.
+template <int SWZ>
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>(1) << 16;             // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;     // SBO
-  d |= static_cast<uint64_t>(1) << 46;             // sm100 descriptor version
-  d |= static_cast<uint64_t>(2) << 61;             // SWIZZLE_128B
+  d |= static_cast<uint64_t>(1) << 16;                  // LBO (ignored when swizzled)
+  d |= static_cast<uint64_t>((8 * SWZ) >> 4) << 32;     // SBO: one 8-row atom
+  d |= static_cast<uint64_t>(1) << 46;                  // sm100 descriptor version
+  d |= static_cast<uint64_t>(SWZ == 128 ? 2 : 4) << 61; // swizzle mode
   return d;
 }
 
@@ -111,57 +138,82 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, int STAGES>
+struct TcParams {
+  int64_t M, N;          // complex rows of A / complex columns of C
+  int num_kb;            // k-blocks over the padded real K
+  int kb_per_split;      // k-blocks per split-K unit
+  int splits;
+  int m_blocks, n_blocks;
+  int group_m;           // raster group height (m-blocks)
+  int kb_per_chunk;      // k-blocks accumulated in TMEM before a register fold
+  float2* C;
+  int64_t ldcm, ldcn;    // complex strides of C[m, n]
+  float2* partials;      // [splits][M][N] when splits > 1
+};
+
+template <int BN, int SWZ, int STAGES>
 struct TcCfg {
-  static constexpr int kABytes = kBM * kBK * 4;     // one A plane tile
-  static constexpr int kBBytes = BN * kBK * 4;      // one B plane tile
+  static constexpr int kBK = SWZ / 4;                // real K per k-block
+  static constexpr int kABytes = kBM * SWZ;          // one A plane tile
+  static constexpr int kBBytes = BN * SWZ;           // one B plane tile
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kSmem = STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  // instruction descriptor: D=f32, A=B=tf32, both K-major, N, M=128
+  static constexpr int kHalf = BN / 2;               // columns per epilogue warp
+  // instruction descriptor: D=f32, A=B=tf32, both K-major, N=BN, M=128
   static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
                                      (static_cast<uint32_t>(BN >> 3) << 17) |
                                      (static_cast<uint32_t>(kBM >> 4) << 24);
 };
 
-template <int BN, int STAGES>
+__device__ __forceinline__ void decode_unit(const TcParams& p, int u, int& split, int& mb, int& nb) {
+  const int tiles = p.m_blocks * p.n_blocks;
+  split = u / tiles;
+  const int t = u - split * tiles;
+  const int span = p.group_m * p.n_blocks;
+  const int g = t / span;
+  const int first_m = g * p.group_m;
+  const int gsize = min(p.group_m, p.m_blocks - first_m);
+  const int r = t - g * span;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int BN, int SWZ, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_cgemm_kernel(const __grid_constant__ CUtensorMap mapAb,
                     const __grid_constant__ CUtensorMap mapAs,
                     const __grid_constant__ CUtensorMap mapBb,
-                    const __grid_constant__ CUtensorMap mapBs, int64_t M, int64_t N,
-                    int num_kb_total, int kb_per_split, float2* __restrict__ C, int64_t ldcm,
-                    int64_t ldcn, float2* __restrict__ partials) {
-  using Cfg = TcCfg<BN, STAGES>;
+                    const __grid_constant__ CUtensorMap mapBs, const TcParams p) {
+  using Cfg = TcCfg<BN, SWZ, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;   // [2] chunk ready in TMEM buffer b
+  uint64_t* tempty = tfull + 2;       // [2] TMEM buffer b drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kBM;
-  const int n0r = blockIdx.x * BN;  // real column (= 2 * complex column)
-  const int split = blockIdx.z;
-  const int kb_lo = split * kb_per_split;
-  const int kb_hi = min(num_kb_total, kb_lo + kb_per_split);
-  const int nkb = kb_hi - kb_lo;
+  const int units = p.m_blocks * p.n_blocks * p.splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(static_cast<uint32_t>(BN)));
+                 "r"(static_cast<uint32_t>(2 * BN)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -172,80 +224,140 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapAb)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapAs)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBb)) : "memory");
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + s * Cfg::kStageBytes;
-        mbar_expect_tx(&full[s], Cfg::kStageBytes);
-        const int kc = (kb_lo + i) * kBK;
-        tma_load_2d(&mapAb, &full[s], st, kc, static_cast<int32_t>(m0));
-        tma_load_2d(&mapAs, &full[s], st + Cfg::kABytes, kc, static_cast<int32_t>(m0));
-        tma_load_2d(&mapBb, &full[s], st + 2 * Cfg::kABytes, kc, n0r);
-        tma_load_2d(&mapBs, &full[s], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc, n0r);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBs)) : "memory");
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int split, mb, nb;
+        decode_unit(p, u, split, mb, nb);
+        const int kb_lo = split * p.kb_per_split;
+        const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * Cfg::kStageBytes;
+          mbar_expect_tx(&full[s], Cfg::kStageBytes);
+          const int kc = kb * Cfg::kBK;
+          tma_load_2d(&mapAb, &full[s], st, kc, mb * kBM);
+          tma_load_2d(&mapAs, &full[s], st + Cfg::kABytes, kc, mb * kBM);
+          tma_load_2d(&mapBb, &full[s], st + 2 * Cfg::kABytes, kc, nb * BN);
+          tma_load_2d(&mapBs, &full[s], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc, nb * BN);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = smem_u32(smem + s * Cfg::kStageBytes);
-        const uint32_t a_big = st, a_small = st + Cfg::kABytes;
-        const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
+      uint32_t it = 0, ch = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int split, mb, nb;
+        decode_unit(p, u, split, mb, nb);
+        const int kb_lo = split * p.kb_per_split;
+        const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+        int in_chunk = 0;
+        uint32_t dcol = 0;
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          if (in_chunk == 0) {
+            const uint32_t b = ch & 1;
+            mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            dcol = tmem_base + b * BN;
+          }
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * Cfg::kStageBytes);
+          const uint32_t a_big = st, a_small = st + Cfg::kABytes;
+          const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
-          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-          const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem_base, sw128_desc(a_small + off), sw128_desc(b_big + off), Cfg::kIdesc,
-                   acc0);
-          mma_tf32(tmem_base, sw128_desc(a_big + off), sw128_desc(b_small + off), Cfg::kIdesc, 1u);
-          mma_tf32(tmem_base, sw128_desc(a_big + off), sw128_desc(b_big + off), Cfg::kIdesc, 1u);
+          for (int kk = 0; kk < Cfg::kBK / 8; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+            const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc,
+                     acc0);
+            mma_tf32(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off), Cfg::kIdesc,
+                     1u);
+            mma_tf32(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc, 1u);
+          }
+          mma_commit(&empty[s]);
+          ++in_chunk;
+          if (in_chunk == p.kb_per_chunk || kb + 1 == kb_hi) {
+            mma_commit(&tfull[ch & 1]);
+            ++ch;
+            in_chunk = 0;
+          }
         }
-        mma_commit(&empty[s]);
       }
-      mma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
+    // chunk reducers + epilogue
     const int quad = warp & 3;
-    const int64_t row = m0 + quad * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    const int64_t ncplx0 = n0r / 2;
-    float2* dst_base;
-    int64_t sm, sn;
-    if (partials != nullptr) {
-      dst_base = partials + static_cast<int64_t>(split) * M * N;
-      sm = N;
-      sn = 1;
-    } else {
-      dst_base = C;
-      sm = ldcm;
-      sn = ldcn;
-    }
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t v[32];
-      tmem_ld32(t_row + c, v);
-      if (row < M && nkb > 0) {
-        float2* drow = dst_base + row * sm;
+    const int half = (warp - 2) >> 2;
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    float acc[Cfg::kHalf];
+    uint32_t ch = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int split, mb, nb;
+      decode_unit(p, u, split, mb, nb);
+      const int kb_lo = split * p.kb_per_split;
+      const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+      const int nchunks = (kb_hi - kb_lo + p.kb_per_chunk - 1) / p.kb_per_chunk;
+      for (int c = 0; c < nchunks; ++c, ++ch) {
+        const uint32_t b = ch & 1;
+        mbar_wait(&tfull[b], (ch >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t taddr = tmem_base + lane_base + b * BN + half * Cfg::kHalf;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int64_t n = ncplx0 + c / 2 + j;
-          if (n < N) drow[n * sn] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        for (int g = 0; g < Cfg::kHalf / 32; ++g) {
+          uint32_t v[32];
+          tmem_ld32(taddr + g * 32, v);
+          if (c == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[g * 32 + j] = __uint_as_float(v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[g * 32 + j] += __uint_as_float(v[j]);
+          }
         }
-      } else if (row < M) {
-        float2* drow = dst_base + row * sm;
-        for (int j = 0; j < 16; ++j) {
-          const int64_t n = ncplx0 + c / 2 + j;
-          if (n < N) drow[n * sn] = make_float2(0.f, 0.f);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+      }
+      if (nchunks == 0) {
+#pragma unroll
+        for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
+      }
+      // store this thread's row: complex columns [ncol0, ncol0 + kHalf/2)
+      const int64_t row = static_cast<int64_t>(mb) * kBM + quad * 32 + lane;
+      if (row < p.M) {
+        const int64_t ncol0 = (static_cast<int64_t>(nb) * BN + half * Cfg::kHalf) / 2;
+        float2* dst;
+        int64_t sm, sn;
+        if (p.splits > 1) {
+          dst = p.partials + static_cast<int64_t>(split) * p.M * p.N;
+          sm = p.N;
+          sn = 1;
+        } else {
+          dst = p.C;
+          sm = p.ldcm;
+          sn = p.ldcn;
+        }
+        float2* drow = dst + row * sm;
+        if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
+          float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 4; ++j)
+            d4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
+            const int64_t n = ncol0 + j;
+            if (n < p.N) drow[n * sn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          }
         }
       }
     }
@@ -254,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(static_cast<uint32_t>(BN)));
+                 "r"(static_cast<uint32_t>(2 * BN)));
   }
 }
 
@@ -268,72 +380,98 @@ EncodeFn get_encode() {
   static EncodeFn fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* p = nullptr;
+    void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
+      fn = reinterpret_cast<EncodeFn>(ptr);
   });
   return fn;
 }
 
-int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols_real, int box_rows) {
+int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols_real, int box_rows,
+             int swz) {
   EncodeFn enc = get_encode();
   if (!enc) TNC_RET(TNC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols_real), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols_real) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(swz / 4), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) TNC_RET(TNC_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return TNC_OK;
 }
 
-template <int BN, int STAGES>
-int launch_cfg(int64_t M, int64_t N, int64_t Kp, const float* Ab, const float* As, const float* Bb,
-               const float* Bs, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+template <int BN, int SWZ, int STAGES>
+int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Ab, const float* As,
+               const float* Bb, const float* Bs, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
                float* partials, cudaStream_t stream) {
-  using Cfg = TcCfg<BN, STAGES>;
+  using Cfg = TcCfg<BN, SWZ, STAGES>;
   const int64_t Kr = 2 * Kp;
   CUtensorMap mAb, mAs, mBb, mBs;
-  TNC_TRY(make_map(&mAb, Ab, M, Kr, kBM));
-  TNC_TRY(make_map(&mAs, As, M, Kr, kBM));
-  TNC_TRY(make_map(&mBb, Bb, 2 * N, Kr, BN));
-  TNC_TRY(make_map(&mBs, Bs, 2 * N, Kr, BN));
-  const int num_kb = static_cast<int>(Kr / kBK);
-  const int splits = std::max(1, std::min(k_splits, num_kb));
-  const int kb_per = static_cast<int>(ceil_div(num_kb, splits));
-  const int real_splits = static_cast<int>(ceil_div(num_kb, kb_per));
-  auto kern = tc_cgemm_kernel<BN, STAGES>;
+  TNC_TRY(make_map(&mAb, Ab, M, Kr, kBM, SWZ));
+  TNC_TRY(make_map(&mAs, As, M, Kr, kBM, SWZ));
+  TNC_TRY(make_map(&mBb, Bb, 2 * N, Kr, BN, SWZ));
+  TNC_TRY(make_map(&mBs, Bs, 2 * N, Kr, BN, SWZ));
+  TcParams p{};
+  p.M = M;
+  p.N = N;
+  p.num_kb = static_cast<int>(Kr / Cfg::kBK);
+  const int splits = std::max(1, std::min(k_splits, p.num_kb));
+  p.kb_per_split = static_cast<int>(ceil_div(p.num_kb, splits));
+  p.splits = static_cast<int>(ceil_div(p.num_kb, p.kb_per_split));
+  p.m_blocks = static_cast<int>(ceil_div(M, kBM));
+  p.n_blocks = static_cast<int>(ceil_div(2 * N, BN));
+  p.group_m = std::max(1, env_int("TNC_GROUP_M", 16));
+  // chunk = 32 complex K per TMEM accumulation chain (see header comment)
+  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", 64 / Cfg::kBK));
+  p.C = static_cast<float2*>(C);
+  p.ldcm = ldcm;
+  p.ldcn = ldcn;
+  p.partials = p.splits > 1 ? reinterpret_cast<float2*>(partials) : nullptr;
+  const int64_t units = static_cast<int64_t>(p.m_blocks) * p.n_blocks * p.splits;
+  if (units > INT32_MAX) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_cgemm: too many tiles");
+  auto kern = tc_cgemm_kernel<BN, SWZ, STAGES>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
-  dim3 grid(static_cast<unsigned>(ceil_div(2 * N, BN)), static_cast<unsigned>(ceil_div(M, kBM)),
-            static_cast<unsigned>(real_splits));
-  if (grid.y > 65535) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_cgemm: M too large for grid");
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mAb, mAs, mBb, mBs, M, N, num_kb, kb_per,
-                                               static_cast<float2*>(C), ldcm, ldcn,
-                                               real_splits > 1 ? reinterpret_cast<float2*>(partials)
-                                                               : nullptr);
-  TNC_CHECK_LAUNCH();
-  if (real_splits > 1)
-    return tree_reduce_launch(TNC_C64, real_splits, M * N, partials, C, M, N, ldcm, ldcn, stream);
+  const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
+  {
+    ProfScope prof(PROF_TC_GEMM, 8.0 * M * N * K,
+                   8.0 * (double(M) * K + double(N) * K + double(M) * N), stream);
+    kern<<<grid, kThreads, Cfg::kSmem, stream>>>(mAb, mAs, mBb, mBs, p);
+    TNC_CHECK_LAUNCH();
+  }
+  if (p.splits > 1)
+    return tree_reduce_launch(TNC_C64, p.splits, M * N, partials, C, M, N, ldcm, ldcn, stream);
   return TNC_OK;
 }
 
 }  // namespace
 
-int tc_cgemm_launch(int64_t M, int64_t N, int64_t Kp, const float* Abig, const float* Asmall,
-                    const float* Bbig, const float* Bsmall, void* C, int64_t ldcm, int64_t ldcn,
-                    int k_splits, float* partials, cudaStream_t stream) {
+int tc_cgemm_launch(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Abig,
+                    const float* Asmall, const float* Bbig, const float* Bsmall, void* C,
+                    int64_t ldcm, int64_t ldcn, int k_splits, float* partials,
+                    cudaStream_t stream) {
   if (M <= 0 || N <= 0) return TNC_OK;
   if (Kp % 16 != 0) TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 16");
-  if (2 * N >= 256)
-    return launch_cfg<256, 2>(M, N, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn, k_splits,
-                              partials, stream);
-  return launch_cfg<128, 3>(M, N, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn, k_splits,
-                            partials, stream);
+  const int cfg = env_int("TNC_TC_CFG", 0);
+  if (2 * N >= 256) {
+    if (cfg == 1)
+      return launch_cfg<256, 128, 2>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn,
+                                     k_splits, partials, stream);
+    return launch_cfg<256, 64, 4>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn,
+                                  k_splits, partials, stream);
+  }
+  return launch_cfg<128, 64, 6>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn, k_splits,
+                                partials, stream);
 }
 
 }  // namespace tnc

@@ -205,6 +205,7 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     ax.swap(merged);
   }
   if (total == 0) return TNC_OK;
+  ProfScope prof(PROF_PERMUTE, 0.0, 2.0 * static_cast<double>(total) * eb, stream);
   // full contiguous copy
   if (ax.empty() || (ax.size() == 1 && ax[0].in_stride == 1)) {
     TNC_CUDA_TRY(cudaMemcpyAsync(out, in, static_cast<size_t>(total) * eb,

