@@ -181,7 +181,7 @@ void build_gather(Operand& op) {
 }
 
 bool tc_eligible(const tnc_plan* p) {
-  return p->dtype == TNC_C64 && p->rows_x >= 128 && p->rows_y >= 32 && p->k >= 32 &&
+  return p->dtype == TNC_C64 && p->rows_x >= 128 && p->rows_y >= 32 && p->k >= 8 &&
          static_cast<__int128>(p->rows_x) * p->rows_y * p->k >= (static_cast<__int128>(1) << 26);
 }
 
@@ -393,12 +393,16 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   // variant
   int want = variant;
-  if (want == TNC_VARIANT_AUTO) want = tc_eligible(p) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_SIMT;
+  if (want == TNC_VARIANT_AUTO) {
+    if (p->rows_x * p->rows_y <= 1024 && k >= 4096)
+      want = TNC_VARIANT_SPLITK;  // tiny output, huge K: CUDA-core split-K reduction
+    else
+      want = tc_eligible(p) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_SIMT;
+  }
   if (want == TNC_VARIANT_TC3XTF32 && p->dtype != TNC_C64) {
     delete p;
     TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
   }
-  if (want == TNC_VARIANT_SPLITK) want = TNC_VARIANT_TC3XTF32;
   p->variant = want;
   p->kp = ((k + 15) / 16) * 16;
   // split-K when the output tile grid cannot fill the machine
@@ -432,6 +436,8 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   p->off_partials = off;
   if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
+  if (p->variant == TNC_VARIANT_SPLITK)
+    off = align_up(off + static_cast<size_t>(splitk_chunks(p->rows_x, p->rows_y, k)) * m * n * eb);
   p->off_tmp = off;
   if (p->custom_out) off = align_up(off + static_cast<size_t>(m) * n * eb);
   p->ws_bytes = off;
@@ -492,6 +498,9 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     return tc_cgemm_launch(p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs, c, ldcm, ldcn, k_splits,
                            reinterpret_cast<float*>(ws + p->off_partials), st);
   }
+  if (p->variant == TNC_VARIANT_SPLITK)
+    return simt_splitk_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ldx, ym, ldy, c, ldcm, ldcn,
+                              ws + p->off_partials, st);
   return simt_cgemm_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ldx, ym, ldy, c, ldcm, ldcn,
                            0, st);
 }

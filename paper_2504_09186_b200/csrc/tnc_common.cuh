@@ -112,6 +112,12 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
 int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
                       const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn,
                       int accumulate, cudaStream_t stream);
+// split-K for tiny M*N, huge K: chunk partials in `parts` ([chunks][M][N]),
+// then the fixed-order tree reduction into C
+int64_t splitk_chunks(int64_t M, int64_t N, int64_t K);
+int simt_splitk_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
+                       const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn, void* parts,
+                       cudaStream_t stream);
 // axpy y += x
 int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream);
 // 3xTF32 prep: split complex X[R, K] (row-major, K contiguous, leading dim ldx)

@@ -159,6 +159,84 @@ __global__ void __launch_bounds__(256) simt_dot_kernel(int64_t M, int64_t N, int
   }
 }
 
+// Split-K for tiny M*N with huge K (e.g. the (2,21,4) closing step of a
+// circuit slice): block (chunk, tile) folds K range [chunk*kc, ...) for a
+// TM x TN output tile; each thread strides over k (coalesced across the warp),
+// keeps TM*TN complex partials in registers, then a fixed-order warp-shuffle +
+// shared-memory reduction produces the block partial [chunk][M][N].
+template <typename T, int TM, int TN>
+__global__ void __launch_bounds__(256) simt_splitk_kernel(int64_t M, int64_t N, int64_t K, int64_t kc,
+                                                          const T* __restrict__ X, int64_t ldx,
+                                                          const T* __restrict__ Y, int64_t ldy,
+                                                          T* __restrict__ parts) {
+  using R = typename real_of<T>::type;
+  const int64_t chunk = blockIdx.x;
+  const int64_t n_tiles_n = (N + TN - 1) / TN;
+  const int64_t m0 = (blockIdx.y / n_tiles_n) * TM;
+  const int64_t n0 = (blockIdx.y % n_tiles_n) * TN;
+  const int64_t k_lo = chunk * kc;
+  const int64_t k_hi = min(K, k_lo + kc);
+  R acc_re[TM][TN], acc_im[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc_re[i][j] = acc_im[i][j] = R(0);
+  for (int64_t k = k_lo + threadIdx.x; k < k_hi; k += blockDim.x) {
+    T x[TM], y[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      if (m0 + i < M) x[i] = X[(m0 + i) * ldx + k];
+      else x[i].re = x[i].im = R(0);
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      if (n0 + j < N) y[j] = Y[(n0 + j) * ldy + k];
+      else y[j].re = y[j].im = R(0);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        acc_re[i][j] = fma(x[i].re, y[j].re, acc_re[i][j]);
+        acc_re[i][j] = fma(-x[i].im, y[j].im, acc_re[i][j]);
+        acc_im[i][j] = fma(x[i].re, y[j].im, acc_im[i][j]);
+        acc_im[i][j] = fma(x[i].im, y[j].re, acc_im[i][j]);
+      }
+  }
+  __shared__ R red[8][TM * TN * 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      R re = acc_re[i][j], im = acc_im[i][j];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, s);
+        im += __shfl_xor_sync(0xffffffffu, im, s);
+      }
+      if (lane == 0) {
+        red[warp][2 * (i * TN + j)] = re;
+        red[warp][2 * (i * TN + j) + 1] = im;
+      }
+    }
+  __syncthreads();
+  for (int o = threadIdx.x; o < TM * TN; o += blockDim.x) {
+    R re = R(0), im = R(0);
+    for (int w = 0; w < 8; ++w) {
+      re += red[w][2 * o];
+      im += red[w][2 * o + 1];
+    }
+    const int i = o / TN, j = o % TN;
+    if (m0 + i < M && n0 + j < N) {
+      T v;
+      v.re = re;
+      v.im = im;
+      parts[chunk * M * N + (m0 + i) * N + (n0 + j)] = v;
+    }
+  }
+}
+
 template <typename T>
 __global__ void axpy_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ y) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -293,6 +371,39 @@ int simt_cgemm_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X,
                                                 static_cast<c64*>(C), ldcm, ldcn, accumulate);
   TNC_CHECK_LAUNCH();
   return TNC_OK;
+}
+
+int64_t splitk_chunks(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(M, 4) * ceil_div(N, 8);
+  int64_t chunks = std::max<int64_t>(1, static_cast<int64_t>(num_sms()) * 4 / std::max<int64_t>(tiles, 1));
+  chunks = std::min<int64_t>(chunks, ceil_div(K, 1024));  // >= 4 k per thread
+  return std::max<int64_t>(chunks, 1);
+}
+
+int simt_splitk_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
+                       const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn, void* parts,
+                       cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return TNC_OK;
+  const int64_t chunks = splitk_chunks(M, N, K);
+  const int64_t kc = ceil_div(K, chunks);
+  const int64_t tiles = ceil_div(M, 4) * ceil_div(N, 8);
+  if (tiles > 65535) TNC_RET(TNC_ERR_UNSUPPORTED, "split-K: output too large");
+  {
+    const double eb = static_cast<double>(elem_bytes(dtype));
+    ProfScope prof(PROF_SIMT_GEMM, 8.0 * M * N * K, eb * (double(M) * K + double(N) * K + double(M) * N),
+                   stream);
+    dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(tiles));
+    if (dtype == TNC_C128)
+      simt_splitk_kernel<c128, 4, 8><<<grid, 256, 0, stream>>>(M, N, K, kc, static_cast<const c128*>(X), ldx,
+                                                               static_cast<const c128*>(Y), ldy,
+                                                               static_cast<c128*>(parts));
+    else
+      simt_splitk_kernel<c64, 4, 8><<<grid, 256, 0, stream>>>(M, N, K, kc, static_cast<const c64*>(X), ldx,
+                                                              static_cast<const c64*>(Y), ldy,
+                                                              static_cast<c64*>(parts));
+    TNC_CHECK_LAUNCH();
+  }
+  return tree_reduce_launch(dtype, chunks, M * N, parts, C, M, N, ldcm, ldcn, stream);
 }
 
 int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream) {

@@ -24,56 +24,68 @@ namespace {
 constexpr int kMaxTile = 2048;  // elements per smem tile
 constexpr int kMaxAxes = 2 * TNC_MAX_RANK;
 
+// Outer (non-tile) axes of a permutation: digit a of a linear outer index id
+// is (id / div[a]) % dim[a]; it moves the input by sin[a], the output by sout[a].
+struct OuterAxes {
+  int n;
+  int64_t dim[kMaxAxes];
+  int64_t div[kMaxAxes];
+  int64_t sin[kMaxAxes];
+  int64_t sout[kMaxAxes];
+};
+
 struct PermParams {
   int n_tile;              // tile axes, ordered by input stride ascending
-  int n_outer;             // outer axes, most significant first
   int tile_elems;
   int64_t n_tiles;
   int64_t tile_dim[16];
   int64_t tile_in[16];
   int64_t tile_out[16];
   int tile_out_rank[16];   // position of tile axis in output-fastest order
-  int64_t outer_dim[kMaxAxes];
-  int64_t outer_in[kMaxAxes];
-  int64_t outer_out[kMaxAxes];
+  OuterAxes outer;
 };
 
 struct RowParams {
-  int n_outer;
   int64_t row_len;
   int64_t n_rows;
-  int64_t outer_dim[kMaxAxes];
-  int64_t outer_in[kMaxAxes];
-  int64_t outer_out[kMaxAxes];
+  OuterAxes outer;
 };
 
-__device__ __forceinline__ void decode_outer(int64_t id, int n, const int64_t* dim,
-                                             const int64_t* sin, const int64_t* sout,
-                                             int64_t& bin, int64_t& bout) {
-  bin = 0;
-  bout = 0;
-  for (int a = n - 1; a >= 0; --a) {
-    int64_t d = dim[a];
-    int64_t q = id / d;
-    int64_t r = id - q * d;
-    id = q;
-    bin += r * sin[a];
-    bout += r * sout[a];
+// Warp-parallel decode of an outer index: lane l handles axes l, l+32, ...,
+// contributions are summed with shuffles.  All lanes return the result.
+__device__ __forceinline__ void warp_decode(int64_t id, const OuterAxes& o, int lane, int64_t& bin,
+                                            int64_t& bout) {
+  int64_t si = 0, so = 0;
+  for (int a = lane; a < o.n; a += 32) {
+    const int64_t digit = (id / o.div[a]) % o.dim[a];
+    si += digit * o.sin[a];
+    so += digit * o.sout[a];
   }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    si += __shfl_xor_sync(0xffffffffu, si, s);
+    so += __shfl_xor_sync(0xffffffffu, so, s);
+  }
+  bin = si;
+  bout = so;
 }
 
 __device__ __forceinline__ int pad_idx(int e) { return e + (e >> 4); }
 
+constexpr int kTileThreads = 256;
+constexpr int kItems = kMaxTile / kTileThreads;  // elements per thread per tile (<= 8)
+
 template <typename T>
-__global__ void __launch_bounds__(256) permute_tile_kernel(const T* __restrict__ in,
-                                                           T* __restrict__ out,
-                                                           const PermParams p) {
+__global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __restrict__ in,
+                                                                    T* __restrict__ out,
+                                                                    const PermParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tiles_pad = pad_idx(p.tile_elems) + 1;
   int64_t* in_off = reinterpret_cast<int64_t*>(tile + tiles_pad);
   int64_t* out_off = in_off + p.tile_elems;
   int* src_of = reinterpret_cast<int*>(out_off + p.tile_elems);
+  __shared__ int64_t s_base[2];
 
   // Build tables once per block.
   // Input-order enumeration e: digits over tile axes, axis 0 fastest.
@@ -115,14 +127,43 @@ __global__ void __launch_bounds__(256) permute_tile_kernel(const T* __restrict__
   }
   __syncthreads();
 
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
   for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-    int64_t bin, bout;
-    decode_outer(t, p.n_outer, p.outer_dim, p.outer_in, p.outer_out, bin, bout);
-    const T* src = in + bin;
-    T* dst = out + bout;
-    for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) tile[pad_idx(e)] = src[in_off[e]];
+    if (tid < 32) {
+      int64_t bin, bout;
+      warp_decode(t, p.outer, lane, bin, bout);
+      if (lane == 0) {
+        s_base[0] = bin;
+        s_base[1] = bout;
+      }
+    }
     __syncthreads();
-    for (int f = threadIdx.x; f < p.tile_elems; f += blockDim.x) dst[out_off[f]] = tile[src_of[f]];
+    const T* src = in + s_base[0];
+    T* dst = out + s_base[1];
+    // batched loads: all of this thread's elements in flight before any store
+    T v[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int e = tid + i * kTileThreads;
+      if (e < p.tile_elems) v[i] = src[in_off[e]];
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int e = tid + i * kTileThreads;
+      if (e < p.tile_elems) tile[pad_idx(e)] = v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int f = tid + i * kTileThreads;
+      if (f < p.tile_elems) v[i] = tile[src_of[f]];
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const int f = tid + i * kTileThreads;
+      if (f < p.tile_elems) dst[out_off[f]] = v[i];
+    }
     __syncthreads();
   }
 }
@@ -137,7 +178,7 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const T* __restrict__
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = warp; r < p.n_rows; r += n_warps) {
     int64_t bin, bout;
-    decode_outer(r, p.n_outer, p.outer_dim, p.outer_in, p.outer_out, bin, bout);
+    warp_decode(r, p.outer, lane, bin, bout);
     const T* src = in + bin;
     T* dst = out + bout;
     int64_t i = lane;
@@ -155,6 +196,21 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const T* __restrict__
 struct NormAxis {
   int64_t dim, in_stride, out_stride;
 };
+
+// outer axes listed most significant first
+int fill_outer(const std::vector<NormAxis>& axes, OuterAxes& o) {
+  if (axes.size() > static_cast<size_t>(kMaxAxes)) TNC_RET(TNC_ERR_TENSOR, "permute: too many legs");
+  o.n = static_cast<int>(axes.size());
+  int64_t div = 1;
+  for (int a = o.n - 1; a >= 0; --a) {
+    o.dim[a] = axes[a].dim;
+    o.div[a] = div;
+    o.sin[a] = axes[a].in_stride;
+    o.sout[a] = axes[a].out_stride;
+    div *= axes[a].dim;
+  }
+  return TNC_OK;
+}
 
 }  // namespace
 
@@ -218,14 +274,9 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
   if (inner.in_stride == 1 && inner.dim >= 16) {
     RowParams p{};
     p.row_len = inner.dim;
-    p.n_outer = static_cast<int>(ax.size()) - 1;
     p.n_rows = total / inner.dim;
-    if (p.n_outer > kMaxAxes) TNC_RET(TNC_ERR_TENSOR, "permute: too many legs");
-    for (int i = 0; i < p.n_outer; ++i) {
-      p.outer_dim[i] = ax[i].dim;
-      p.outer_in[i] = ax[i].in_stride;
-      p.outer_out[i] = ax[i].out_stride;
-    }
+    std::vector<NormAxis> outer(ax.begin(), ax.end() - 1);
+    TNC_TRY(fill_outer(outer, p.outer));
     int64_t warps_needed = p.n_rows;
     int64_t blocks = std::min<int64_t>(ceil_div(warps_needed, 8), static_cast<int64_t>(sms) * 16);
     blocks = std::max<int64_t>(blocks, 1);
@@ -298,6 +349,25 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     }
     if (!progressed) break;
   }
+  // then grow the tile (alternating input- / output-fastest legs) up to
+  // kMaxTile elements: more bytes per block barrier, more loads in flight
+  {
+    size_t qi = 0, qo = 0;
+    bool grew = true;
+    while (grew) {
+      grew = false;
+      while (qi < by_in.size() && in_tile[by_in[qi]]) ++qi;
+      if (qi < by_in.size() && tile * ax[by_in[qi]].dim <= kMaxTile) {
+        try_add(by_in[qi]);
+        grew = true;
+      }
+      while (qo < by_out.size() && in_tile[by_out[qo]]) ++qo;
+      if (qo < by_out.size() && tile * ax[by_out[qo]].dim <= kMaxTile) {
+        try_add(by_out[qo]);
+        grew = true;
+      }
+    }
+  }
   if (tile == 1) {
     // every leg is huge and unsplittable: degenerate to one-element tiles
     in_tile[by_out[0]] = 1;
@@ -322,21 +392,17 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
       ++nt;
     }
   p.n_tile = nt;
-  int no = 0;
-  for (int a = 0; a < n; ++a)
-    if (!in_tile[a]) {
-      if (no >= kMaxAxes) TNC_RET(TNC_ERR_TENSOR, "permute: too many legs");
-      p.outer_dim[no] = ax[a].dim;
-      p.outer_in[no] = ax[a].in_stride;
-      p.outer_out[no] = ax[a].out_stride;
-      ++no;
-    }
-  p.n_outer = no;
+  {
+    std::vector<NormAxis> outer;
+    for (int a = 0; a < n; ++a)
+      if (!in_tile[a]) outer.push_back(ax[a]);
+    TNC_TRY(fill_outer(outer, p.outer));
+  }
   p.n_tiles = total / tile;
   const int tiles_pad = (p.tile_elems + (p.tile_elems >> 4)) + 1;
   size_t smem = static_cast<size_t>(tiles_pad) * eb + static_cast<size_t>(p.tile_elems) * 20;
   smem = (smem + 15) & ~size_t(15);
-  int blocks_per_sm = tile >= 1024 ? 2 : 4;
+  int blocks_per_sm = tile >= 1024 ? 3 : 6;
   int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(sms) * blocks_per_sm);
   if (dtype == TNC_C128) {
     auto k = permute_tile_kernel<c128>;

@@ -90,10 +90,25 @@ def test_permute_mixed_dims_and_projected_views(cuda_ready):
     assert np.array_equal(got, want)
 
 
-VARIANTS = {"auto": 0, "simt": 1, "tc": 2}
+VARIANTS = {"auto": 0, "simt": 1, "tc": 2, "splitk": 3}
 
 
-@pytest.mark.parametrize("variant", ["auto", "simt", "tc"])
+@pytest.mark.parametrize("m,n,k", [(4, 16, 1 << 21), (1, 1, 1 << 16), (3, 5, 10000), (32, 32, 8192)])
+def test_splitk_small_output_vs_torch_fp64(cuda_ready, m, n, k):
+    """CUDA-core split-K (tiny M*N, huge K) vs a torch complex128 reference."""
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair
+
+    g = torch.Generator(device="cuda").manual_seed(m * n + k)
+    a = torch.randn((m, k), dtype=torch.complex64, device="cuda", generator=g)
+    b = torch.randn((k, n), dtype=torch.complex64, device="cuda", generator=g)
+    got = contract_pair(DenseTensor([Index("m", m), Index("k", k)], a),
+                        DenseTensor([Index("k", k), Index("n", n)], b), variant=3).data
+    want = a.to(torch.complex128) @ b.to(torch.complex128)
+    err = (got.to(torch.complex128) - want).norm() / want.norm()
+    assert err.item() <= 1e-6, err.item()
+
+
+@pytest.mark.parametrize("variant", ["auto", "simt", "tc", "splitk"])
 def test_contract_pair_golden(cuda_ready, variant):
     from paper_2504_09186_b200 import DenseTensor, contract_pair
 
