@@ -64,7 +64,9 @@ typedef enum tnc_variant {
   TNC_VARIANT_AUTO = 0,
   TNC_VARIANT_SIMT = 1,        /* CUDA-core complex GEMM (fp32 / fp64 accumulate) */
   TNC_VARIANT_TC3XTF32 = 2,    /* tcgen05 kind::tf32, 3xTF32 split, TMEM accum    */
-  TNC_VARIANT_SPLITK = 3       /* CUDA-core split-K, fixed-order tree (tiny M*N)  */
+  TNC_VARIANT_SPLITK = 3,      /* CUDA-core split-K, fixed-order tree (tiny M*N)  */
+  TNC_VARIANT_TC3XF16 = 4      /* tcgen05 kind::f16, 2-piece FP16 split with
+                                  per-row power-of-two scaling, TMEM accum        */
 } tnc_variant;
 
 /* A labeled operand: leg i has label id labels[i], extent dims[i], element

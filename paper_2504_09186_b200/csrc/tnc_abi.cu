@@ -180,6 +180,12 @@ void build_gather(Operand& op) {
   }
 }
 
+// 3xFP16 (2x-rate kind::f16, half the operand bytes) unless TNC_TC_TF32=1
+int default_tc_variant() {
+  const char* v = std::getenv("TNC_TC_TF32");
+  return (v && std::atoi(v) != 0) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_TC3XF16;
+}
+
 bool tc_eligible(const tnc_plan* p) {
   return p->dtype == TNC_C64 && p->rows_x >= 128 && p->rows_y >= 32 && p->k >= 8 &&
          static_cast<__int128>(p->rows_x) * p->rows_y * p->k >= (static_cast<__int128>(1) << 26);
@@ -397,20 +403,21 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     if (p->rows_x * p->rows_y <= 1024 && k >= 4096)
       want = TNC_VARIANT_SPLITK;  // tiny output, huge K: CUDA-core split-K reduction
     else
-      want = tc_eligible(p) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_SIMT;
+      want = tc_eligible(p) ? default_tc_variant() : TNC_VARIANT_SIMT;
   }
-  if (want == TNC_VARIANT_TC3XTF32 && p->dtype != TNC_C64) {
+  const bool tc = want == TNC_VARIANT_TC3XTF32 || want == TNC_VARIANT_TC3XF16;
+  if (tc && p->dtype != TNC_C64) {
     delete p;
     TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
   }
   p->variant = want;
-  p->kp = ((k + 15) / 16) * 16;
+  p->kp = ((k + 31) / 32) * 32;
   // split-K when the output tile grid cannot fill the machine
   p->k_splits = 1;
-  if (p->variant == TNC_VARIANT_TC3XTF32) {
+  if (tc) {
     const int64_t bn = (2 * p->rows_y >= 256) ? 256 : 128;
     const int64_t tiles = ceil_div(2 * p->rows_y, bn) * ceil_div(p->rows_x, 128);
-    const int64_t kblocks = 2 * p->kp / 32;
+    const int64_t kblocks = 2 * p->kp / 64;
     const int sms = num_sms();
     if (tiles < sms && kblocks >= 8) {
       int64_t want_splits = std::min<int64_t>(sms / tiles, kblocks / 4);
@@ -429,10 +436,11 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   p->off_y = off;
   if (!Y.in_place) off = align_up(off + static_cast<size_t>(p->rows_y) * k * eb);
   p->off_planes = off;
-  if (p->variant == TNC_VARIANT_TC3XTF32) {
-    const size_t a_plane = static_cast<size_t>(p->rows_x) * 2 * p->kp * 4;
-    const size_t b_plane = static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * 4;
-    off = align_up(off + 2 * a_plane + 2 * b_plane);
+  if (tc) {
+    const size_t pe = p->variant == TNC_VARIANT_TC3XF16 ? 2 : 4;
+    const size_t a_plane = align_up(static_cast<size_t>(p->rows_x) * 2 * p->kp * pe);
+    const size_t b_plane = align_up(static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * pe);
+    off = align_up(off + 2 * a_plane + 2 * b_plane + align_up(4 * p->rows_x) + 4 * p->rows_y);
   }
   p->off_partials = off;
   if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
@@ -486,16 +494,26 @@ static int prep_operand(const tnc_plan* p, const Operand& op, const void* src, u
 static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* ym, int64_t ldy,
                     void* c, int64_t ldcm, int64_t ldcn, uint8_t* ws, int k_splits,
                     cudaStream_t st) {
-  if (p->variant == TNC_VARIANT_TC3XTF32) {
-    const size_t a_plane = static_cast<size_t>(p->rows_x) * 2 * p->kp * 4;
-    const size_t b_plane = static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * 4;
-    float* ab = reinterpret_cast<float*>(ws + p->off_planes);
-    float* as = reinterpret_cast<float*>(ws + p->off_planes + a_plane);
-    float* bb = reinterpret_cast<float*>(ws + p->off_planes + 2 * a_plane);
-    float* bs = reinterpret_cast<float*>(ws + p->off_planes + 2 * a_plane + b_plane);
-    TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
-    TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));
-    return tc_cgemm_launch(p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs, c, ldcm, ldcn, k_splits,
+  if (p->variant == TNC_VARIANT_TC3XTF32 || p->variant == TNC_VARIANT_TC3XF16) {
+    const bool f16 = p->variant == TNC_VARIANT_TC3XF16;
+    const size_t pe = f16 ? 2 : 4;
+    const size_t a_plane = align_up(static_cast<size_t>(p->rows_x) * 2 * p->kp * pe);
+    const size_t b_plane = align_up(static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * pe);
+    uint8_t* ab = ws + p->off_planes;
+    uint8_t* as = ab + a_plane;
+    uint8_t* bb = as + a_plane;
+    uint8_t* bs = bb + b_plane;
+    int* ex = reinterpret_cast<int*>(bs + b_plane);
+    int* ey = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ex) + align_up(4 * p->rows_x));
+    if (f16) {
+      TNC_TRY(f16_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, ex, st));
+      TNC_TRY(f16_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, ey, st));
+    } else {
+      TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
+      TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));
+    }
+    return tc_cgemm_launch(f16 ? 1 : 0, p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs,
+                           f16 ? ex : nullptr, f16 ? ey : nullptr, c, ldcm, ldcn, k_splits,
                            reinterpret_cast<float*>(ws + p->off_partials), st);
   }
   if (p->variant == TNC_VARIANT_SPLITK)

@@ -2,6 +2,7 @@
 // small device utilities.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -126,10 +127,17 @@ int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t strea
 // 2r+1: (im, re)).  Columns >= 2K are zero.
 int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
                       void* big, void* small, cudaStream_t stream);
-// tcgen05 3xTF32 complex GEMM on prepared planes (see tnc_gemm_tc.cu)
-int tc_cgemm_launch(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Abig, const float* Asmall,
-                    const float* Bbig, const float* Bsmall, void* C, int64_t ldcm, int64_t ldcn,
-                    int k_splits, float* partials, cudaStream_t stream);
+// 3xFP16 prep: per-row power-of-two scaled hi/lo fp16 planes (same shapes as
+// tf32_split_launch, 2-byte elements) + per-row scale exponents
+int f16_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
+                     void* hi, void* lo, int* exps, cudaStream_t stream);
+// tcgen05 complex GEMM on prepared planes (see tnc_gemm_tc.cu).  f16 = 0:
+// 3xTF32 fp32 planes; f16 = 1: 3xFP16 half planes with row/column scale
+// exponents ex (rows of A) / ey (complex columns of C).
+int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Abig,
+                    const void* Asmall, const void* Bbig, const void* Bsmall, const int* ex,
+                    const int* ey, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
+                    float* partials, cudaStream_t stream);
 // fixed-order pairwise tree reduction of P partial [M,N] fp32-complex buffers
 int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out_or_null,
                        int64_t M, int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream);

@@ -294,6 +294,59 @@ __global__ void tf32_split_kernel(int mode, int64_t R, int64_t K, int64_t Kp,
   }
 }
 
+// 2-piece FP16 operand planes with a power-of-two scale per row ("3xFP16"):
+//   row r is scaled by 2^-e[r] so its largest |component| lies in [0.5, 1),
+//   hi = fp16(x), lo = fp16(x - hi); then x = 2^e (hi + lo) to ~2^-25 of the
+//   row maximum (fp16 subnormals cover the tail), and
+//   x*y ~= hi*hi' + hi*lo' + lo*hi' keeps fp32-class accuracy relative to the
+//   row/column norms with half the operand bytes of 3xTF32 and the 2x-rate
+//   kind::f16 tensor-core path.  One warp per row.
+// mode 0: planes [R, 2*Kp] (interleaved re, im);  mode 1: expanded [2R, 2*Kp]
+// with rows 2r = (re, -im), 2r+1 = (im, re).  e[r] is written to `exps`.
+__global__ void __launch_bounds__(256) f16_split_kernel(int mode, int64_t R, int64_t K, int64_t Kp,
+                                                        const c64* __restrict__ X, int64_t ldx,
+                                                        __half* __restrict__ hi, __half* __restrict__ lo,
+                                                        int* __restrict__ exps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
+    const c64* row = X + r * ldx;
+    float mx = 0.f;
+    for (int64_t k = lane; k < K; k += 32) {
+      c64 v = row[k];
+      mx = fmaxf(mx, fmaxf(fabsf(v.re), fabsf(v.im)));
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    int e = 0;
+    if (mx > 0.f && isfinite(mx)) frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+    if (lane == 0) exps[r] = e;
+    const float sc = ldexpf(1.f, -e);
+    for (int64_t k = lane; k < Kp; k += 32) {
+      float re = 0.f, im = 0.f;
+      if (k < K) {
+        c64 v = row[k];
+        re = v.re * sc;
+        im = v.im * sc;
+      }
+      const __half hre = __float2half_rn(re), him = __float2half_rn(im);
+      const __half lre = __float2half_rn(re - __half2float(hre));
+      const __half lim = __float2half_rn(im - __half2float(him));
+      if (mode == 0) {
+        reinterpret_cast<__half2*>(hi)[r * Kp + k] = __halves2half2(hre, him);
+        reinterpret_cast<__half2*>(lo)[r * Kp + k] = __halves2half2(lre, lim);
+      } else {
+        __half2* h0 = reinterpret_cast<__half2*>(hi) + (2 * r) * Kp + k;
+        __half2* l0 = reinterpret_cast<__half2*>(lo) + (2 * r) * Kp + k;
+        h0[0] = __halves2half2(hre, __hneg(him));
+        l0[0] = __halves2half2(lre, __hneg(lim));
+        h0[Kp] = __halves2half2(him, hre);
+        l0[Kp] = __halves2half2(lim, lre);
+      }
+    }
+  }
+}
+
 // Fixed-order pairwise tree over P partial tiles [P][MN] (complex, fp32 or
 // fp64): level by level, partial i += partial i+stride, exactly the
 // left-complete combine of contract.py:200-207.  The root is written to
@@ -425,6 +478,18 @@ int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X,
   tf32_split_kernel<<<grid_for(R * Kp), 256, 0, stream>>>(
       mode, R, K, Kp, static_cast<const c64*>(X), ldx, static_cast<float*>(big),
       static_cast<float*>(small));
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+int f16_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
+                     void* hi, void* lo, int* exps, cudaStream_t stream) {
+  if (R <= 0 || Kp <= 0) return TNC_OK;
+  ProfScope prof(PROF_SPLIT_PREP, 0.0, 8.0 * R * K + (mode ? 16.0 : 8.0) * R * Kp, stream);
+  const int64_t blocks = std::min<int64_t>(ceil_div(R, 8), static_cast<int64_t>(num_sms()) * 16);
+  f16_split_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(
+      mode, R, K, Kp, static_cast<const c64*>(X), ldx, static_cast<__half*>(hi), static_cast<__half*>(lo),
+      exps);
   TNC_CHECK_LAUNCH();
   return TNC_OK;
 }

@@ -106,15 +106,26 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+template <bool F16>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  if constexpr (F16) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -149,18 +160,23 @@ struct TcParams {
   float2* C;
   int64_t ldcm, ldcn;    // complex strides of C[m, n]
   float2* partials;      // [splits][M][N] when splits > 1
+  const int* ex;         // 3xFP16: per-row scale exponent of A (nullptr for TF32)
+  const int* ey;         // 3xFP16: per-complex-column scale exponent of B
 };
 
-template <int BN, int SWZ, int STAGES>
+template <int BN, int SWZ, int STAGES, bool F16>
 struct TcCfg {
-  static constexpr int kBK = SWZ / 4;                // real K per k-block
-  static constexpr int kABytes = kBM * SWZ;          // one A plane tile
-  static constexpr int kBBytes = BN * SWZ;           // one B plane tile
+  static constexpr int kElem = F16 ? 2 : 4;         // bytes per plane element
+  static constexpr int kBK = SWZ / kElem;           // real K per k-block
+  static constexpr int kABytes = kBM * SWZ;         // one A plane tile
+  static constexpr int kBBytes = BN * SWZ;          // one B plane tile
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kSmem = STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int kHalf = BN / 2;               // columns per epilogue warp
-  // instruction descriptor: D=f32, A=B=tf32, both K-major, N=BN, M=128
-  static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
+  static constexpr int kHalf = BN / 2;              // columns per epilogue warp
+  static constexpr int kMmaPerKb = SWZ / 32;        // one MMA consumes 32 bytes of K
+  // instruction descriptor: D=f32, A=B=tf32 (2) or f16 (0), K-major, N=BN, M=128
+  static constexpr uint32_t kFmt = F16 ? 0u : 2u;
+  static constexpr uint32_t kIdesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) |
                                      (static_cast<uint32_t>(BN >> 3) << 17) |
                                      (static_cast<uint32_t>(kBM >> 4) << 24);
 };
@@ -178,13 +194,13 @@ __device__ __forceinline__ void decode_unit(const TcParams& p, int u, int& split
   nb = r / gsize;
 }
 
-template <int BN, int SWZ, int STAGES>
+template <int BN, int SWZ, int STAGES, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_cgemm_kernel(const __grid_constant__ CUtensorMap mapAb,
                     const __grid_constant__ CUtensorMap mapAs,
                     const __grid_constant__ CUtensorMap mapBb,
                     const __grid_constant__ CUtensorMap mapBs, const TcParams p) {
-  using Cfg = TcCfg<BN, SWZ, STAGES>;
+  using Cfg = TcCfg<BN, SWZ, STAGES, F16>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -273,14 +289,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a_big = st, a_small = st + Cfg::kABytes;
           const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kBK / 8; ++kk) {
-            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+          for (int kk = 0; kk < Cfg::kMmaPerKb; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 / 16 f16 = 32 bytes along the swizzled row
             const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc,
+            mma_issue<F16>(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc,
                      acc0);
-            mma_tf32(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off), Cfg::kIdesc,
+            mma_issue<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off), Cfg::kIdesc,
                      1u);
-            mma_tf32(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc, 1u);
+            mma_issue<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc, 1u);
           }
           mma_commit(&empty[s]);
           ++in_chunk;
@@ -347,6 +363,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           sn = p.ldcn;
         }
         float2* drow = dst + row * sm;
+        if constexpr (F16) {
+          // undo the per-row / per-column power-of-two operand scaling
+          const int er = p.ex[row];
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
+            const int64_t n = ncol0 + j;
+            const float s = ldexpf(1.f, er + (n < p.N ? p.ey[n] : 0));
+            acc[2 * j] *= s;
+            acc[2 * j + 1] *= s;
+          }
+        }
         if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
           float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
 #pragma unroll
@@ -390,15 +417,16 @@ EncodeFn get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols_real, int box_rows,
-             int swz) {
+int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols_real, int box_rows,
+             int swz, int elem) {
   EncodeFn enc = get_encode();
   if (!enc) TNC_RET(TNC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols_real), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols_real) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(swz / 4), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols_real) * elem};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(swz / elem), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+  CUresult r = enc(map, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -411,17 +439,17 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <int BN, int SWZ, int STAGES>
-int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Ab, const float* As,
-               const float* Bb, const float* Bs, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
-               float* partials, cudaStream_t stream) {
-  using Cfg = TcCfg<BN, SWZ, STAGES>;
+template <int BN, int SWZ, int STAGES, bool F16>
+int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, const void* As,
+               const void* Bb, const void* Bs, const int* ex, const int* ey, void* C, int64_t ldcm,
+               int64_t ldcn, int k_splits, float* partials, cudaStream_t stream) {
+  using Cfg = TcCfg<BN, SWZ, STAGES, F16>;
   const int64_t Kr = 2 * Kp;
   CUtensorMap mAb, mAs, mBb, mBs;
-  TNC_TRY(make_map(&mAb, Ab, M, Kr, kBM, SWZ));
-  TNC_TRY(make_map(&mAs, As, M, Kr, kBM, SWZ));
-  TNC_TRY(make_map(&mBb, Bb, 2 * N, Kr, BN, SWZ));
-  TNC_TRY(make_map(&mBs, Bs, 2 * N, Kr, BN, SWZ));
+  TNC_TRY(make_map(&mAb, Ab, M, Kr, kBM, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mAs, As, M, Kr, kBM, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mBb, Bb, 2 * N, Kr, BN, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mBs, Bs, 2 * N, Kr, BN, SWZ, Cfg::kElem));
   TcParams p{};
   p.M = M;
   p.N = N;
@@ -438,9 +466,11 @@ int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Ab, con
   p.ldcm = ldcm;
   p.ldcn = ldcn;
   p.partials = p.splits > 1 ? reinterpret_cast<float2*>(partials) : nullptr;
+  p.ex = ex;
+  p.ey = ey;
   const int64_t units = static_cast<int64_t>(p.m_blocks) * p.n_blocks * p.splits;
   if (units > INT32_MAX) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_cgemm: too many tiles");
-  auto kern = tc_cgemm_kernel<BN, SWZ, STAGES>;
+  auto kern = tc_cgemm_kernel<BN, SWZ, STAGES, F16>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
   {
@@ -456,22 +486,27 @@ int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Ab, con
 
 }  // namespace
 
-int tc_cgemm_launch(int64_t M, int64_t N, int64_t K, int64_t Kp, const float* Abig,
-                    const float* Asmall, const float* Bbig, const float* Bsmall, void* C,
-                    int64_t ldcm, int64_t ldcn, int k_splits, float* partials,
-                    cudaStream_t stream) {
+int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Abig,
+                    const void* Asmall, const void* Bbig, const void* Bsmall, const int* ex,
+                    const int* ey, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
+                    float* partials, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return TNC_OK;
-  if (Kp % 16 != 0) TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 16");
+  if (Kp % 32 != 0) TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 32");
   const int cfg = env_int("TNC_TC_CFG", 0);
-  if (2 * N >= 256) {
-    if (cfg == 1)
-      return launch_cfg<256, 128, 2>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn,
-                                     k_splits, partials, stream);
-    return launch_cfg<256, 64, 4>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn,
-                                  k_splits, partials, stream);
+#define TNC_TC_ARGS M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, ex, ey, C, ldcm, ldcn, k_splits, partials, stream
+  if (f16) {
+    if (2 * N >= 256) {
+      if (cfg == 1) return launch_cfg<256, 64, 4, true>(TNC_TC_ARGS);
+      return launch_cfg<256, 128, 2, true>(TNC_TC_ARGS);
+    }
+    return launch_cfg<128, 128, 3, true>(TNC_TC_ARGS);
   }
-  return launch_cfg<128, 64, 6>(M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, C, ldcm, ldcn, k_splits,
-                                partials, stream);
+  if (2 * N >= 256) {
+    if (cfg == 1) return launch_cfg<256, 128, 2, false>(TNC_TC_ARGS);
+    return launch_cfg<256, 64, 4, false>(TNC_TC_ARGS);
+  }
+  return launch_cfg<128, 64, 6, false>(TNC_TC_ARGS);
+#undef TNC_TC_ARGS
 }
 
 }  // namespace tnc

@@ -295,11 +295,12 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     for (auto& a : ax) {
       NormAxis cur = a;
       std::vector<NormAxis> parts;  // least significant first
-      while (cur.dim > 64 && cur.dim % 64 == 0) {
-        parts.push_back({64, cur.in_stride, cur.out_stride});
-        cur.in_stride *= 64;
-        cur.out_stride *= 64;
-        cur.dim /= 64;
+      // factors of 32: a 32x32 transpose tile still fits twice in kMaxTile
+      while (cur.dim > 32 && cur.dim % 32 == 0) {
+        parts.push_back({32, cur.in_stride, cur.out_stride});
+        cur.in_stride *= 32;
+        cur.out_stride *= 32;
+        cur.dim /= 32;
       }
       parts.push_back(cur);
       for (auto it = parts.rbegin(); it != parts.rend(); ++it) split.push_back(*it);
