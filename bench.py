@@ -285,8 +285,21 @@ def bench_c3(args) -> None:
 
     if rank == 0:
         peaks = measured_peaks()
-        tf32 = measure_tf32_peak()
-        p_eff = tf32["tf32_tflops"] / 3.0
+        if os.environ.get("TNC_TC_TF32", "0") not in ("", "0"):
+            tf32 = measure_tf32_peak()
+            p_eff = tf32["tf32_tflops"] / 3.0
+            kernel_name = "tc_cgemm_kernel<.., F16=false> (3xTF32 tcgen05.mma kind::tf32)"
+            peak_source = (f"measured cuBLAS TF32 {tf32['tf32_tflops']:.0f} TF/s (burst) / 3 products; "
+                           "MEASURED_PEAKS.json has no TF32 entry")
+            dtype = "c64 (3xTF32 tensor-core GEMM, fp32 accumulate)"
+        else:
+            # 3xFP16: three fp16 tensor-core products per complex-GEMM flop pair;
+            # fp16 dense rate == bf16 dense rate, sustained (kernel runs inside a long step)
+            p_eff = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 3.0
+            kernel_name = "tc_cgemm_kernel<.., F16=true> (3xFP16 tcgen05.mma kind::f16)"
+            peak_source = (f"MEASURED_PEAKS.json bf16_tflops_sustained {peaks.get('bf16_tflops_sustained')} "
+                           "TF/s (fp16 rate) / 3 products")
+            dtype = "c64 (3xFP16 tensor-core GEMM, fp32 accumulate)"
         tc = prof["tc_gemm"]
         achieved = tc["flops"] / (tc["ms"] / 1e3) / 1e12 if tc["ms"] > 0 else None
         cpu = None
@@ -303,7 +316,7 @@ def bench_c3(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (3xTF32 tensor-core GEMM, fp32 accumulate)",
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (seeded 6x6 grid random circuit, SURVEY Appendix A)",
             "config": {"workload": "C3: 6x6 grid, 14 cycles, seed 0, 64 open amplitudes (q30-35), greedy path "
                                    "seed 0, slices to rank<=30 (9 labels, 512 slices)",
@@ -313,12 +326,11 @@ def bench_c3(args) -> None:
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_eff, "unit": "TFLOP/s",
                          "frac": (achieved / p_eff) if achieved else None, "traffic": None,
-                         "kernel": "tc_cgemm_kernel (3xTF32 tcgen05)",
-                         "peak_source": f"measured cuBLAS TF32 {tf32['tf32_tflops']:.0f} TF/s / 3 (3xTF32); "
-                                        "MEASURED_PEAKS.json has no TF32 entry",
+                         "kernel": kernel_name, "peak_source": peak_source,
                          "launches": tc["launches"], "share_of_step": tc["ms"] / 1e3 / elapsed},
             "kernels": prof, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
-            "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "tf32_tflops": tf32["tf32_tflops"]},
+            "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops"),
+                      "bf16_tflops_sustained": peaks.get("bf16_tflops_sustained")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

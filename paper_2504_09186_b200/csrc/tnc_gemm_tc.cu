@@ -397,6 +397,318 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// 2-CTA variant (cta_group::2): a CTA pair computes a 256 x BN tile; each CTA
+// stages its own 128 A rows and HALF of the B tile (BN/2 rows), so per-SM
+// operand traffic (smem writes, L2 reads) drops by a third and the leader's
+// single-thread MMA issue drives both SMs' tensor cores.
+//   leader (rank 0): TMA producer, MMA issuer, epilogue of rows 0..127
+//   peer   (rank 1): TMA producer (signals the leader's barrier), epilogue of
+//                    rows 128..255 (its own TMEM half)
+// ============================================================================
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x989680)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t spin = 0; !mbar_try_cluster(addr, parity); ++spin) {
+    if (spin > (1u << 24)) __trap();
+  }
+}
+
+// TMA load into this CTA's smem whose completion is counted on the LEADER's
+// barrier (peer bit cleared), as the 2-SM MMA consumes both CTAs' tiles.
+__device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                int32_t c0, int32_t c1) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <bool F16>
+__device__ __forceinline__ void mma_issue_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  if constexpr (F16) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int BN, int SWZ, int STAGES, bool F16>
+struct Tc2Cfg {
+  static constexpr int kElem = F16 ? 2 : 4;
+  static constexpr int kBK = SWZ / kElem;
+  static constexpr int kABytes = kBM * SWZ;          // own 128 rows of one A plane
+  static constexpr int kBBytes = (BN / 2) * SWZ;     // own half of one B plane
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kSmem = STAGES * kStageBytes + 1024 + 256;
+  static constexpr int kHalf = BN / 2;
+  static constexpr int kMmaPerKb = SWZ / 32;
+  static constexpr uint32_t kFmt = F16 ? 0u : 2u;
+  static constexpr uint32_t kIdesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) |
+                                     (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(256 >> 4) << 24);
+};
+
+template <int BN, int SWZ, int STAGES, bool F16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_cgemm_2sm_kernel(const __grid_constant__ CUtensorMap mapAb,
+                        const __grid_constant__ CUtensorMap mapAs,
+                        const __grid_constant__ CUtensorMap mapBb,
+                        const __grid_constant__ CUtensorMap mapBs, const TcParams p) {
+  using Cfg = Tc2Cfg<BN, SWZ, STAGES, F16>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int units = p.m_blocks * p.n_blocks * p.splits;  // m_blocks of 256 rows
+  const int pair = blockIdx.x >> 1;
+  const int pairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(static_cast<uint32_t>(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = pair; u < units; u += pairs) {
+        int split, mb, nb;
+        decode_unit(p, u, split, mb, nb);
+        const int kb_lo = split * p.kb_per_split;
+        const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+        const int arow = mb * 256 + static_cast<int>(rank) * kBM;
+        const int brow = nb * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * Cfg::kStageBytes;
+          if (leader) mbar_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+          const int kc = kb * Cfg::kBK;
+          tma_load_2d_2sm(&mapAb, &full[s], st, kc, arow);
+          tma_load_2d_2sm(&mapAs, &full[s], st + Cfg::kABytes, kc, arow);
+          tma_load_2d_2sm(&mapBb, &full[s], st + 2 * Cfg::kABytes, kc, brow);
+          tma_load_2d_2sm(&mapBs, &full[s], st + 2 * Cfg::kABytes + Cfg::kBBytes, kc, brow);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      uint32_t it = 0, ch = 0;
+      for (int u = pair; u < units; u += pairs) {
+        int split, mb, nb;
+        decode_unit(p, u, split, mb, nb);
+        const int kb_lo = split * p.kb_per_split;
+        const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+        int in_chunk = 0;
+        uint32_t dcol = 0;
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          if (in_chunk == 0) {
+            const uint32_t b = ch & 1;
+            mbar_wait_cluster(&tempty[b], ((ch >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            dcol = tmem_base + b * BN;
+          }
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * Cfg::kStageBytes);
+          const uint32_t a_big = st, a_small = st + Cfg::kABytes;
+          const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
+#pragma unroll
+          for (int kk = 0; kk < Cfg::kMmaPerKb; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
+            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off),
+                               Cfg::kIdesc, acc0);
+            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off),
+                               Cfg::kIdesc, 1u);
+            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off),
+                               Cfg::kIdesc, 1u);
+          }
+          mma_commit_2sm(&empty[s]);
+          ++in_chunk;
+          if (in_chunk == p.kb_per_chunk || kb + 1 == kb_hi) {
+            mma_commit_2sm(&tfull[ch & 1]);
+            ++ch;
+            in_chunk = 0;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    float acc[Cfg::kHalf];
+    uint32_t ch = 0;
+    for (int u = pair; u < units; u += pairs) {
+      int split, mb, nb;
+      decode_unit(p, u, split, mb, nb);
+      const int kb_lo = split * p.kb_per_split;
+      const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+      const int nchunks = (kb_hi - kb_lo + p.kb_per_chunk - 1) / p.kb_per_chunk;
+      for (int c = 0; c < nchunks; ++c, ++ch) {
+        const uint32_t b = ch & 1;
+        mbar_wait(&tfull[b], (ch >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t taddr = tmem_base + lane_base + b * BN + half * Cfg::kHalf;
+#pragma unroll
+        for (int g = 0; g < Cfg::kHalf / 32; ++g) {
+          uint32_t v[32];
+          tmem_ld32(taddr + g * 32, v);
+          if (c == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[g * 32 + j] = __uint_as_float(v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[g * 32 + j] += __uint_as_float(v[j]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(map_to_rank(smem_u32(&tempty[b]), 0));
+      }
+      if (nchunks == 0) {
+#pragma unroll
+        for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
+      }
+      const int64_t row = static_cast<int64_t>(mb) * 256 + rank * kBM + quad * 32 + lane;
+      if (row < p.M) {
+        const int64_t ncol0 = (static_cast<int64_t>(nb) * BN + half * Cfg::kHalf) / 2;
+        float2* dst;
+        int64_t sm, sn;
+        if (p.splits > 1) {
+          dst = p.partials + static_cast<int64_t>(split) * p.M * p.N;
+          sm = p.N;
+          sn = 1;
+        } else {
+          dst = p.C;
+          sm = p.ldcm;
+          sn = p.ldcn;
+        }
+        float2* drow = dst + row * sm;
+        if constexpr (F16) {
+          const int er = p.ex[row];
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
+            const int64_t n = ncol0 + j;
+            const float s = ldexpf(1.f, er + (n < p.N ? p.ey[n] : 0));
+            acc[2 * j] *= s;
+            acc[2 * j + 1] *= s;
+          }
+        }
+        if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
+          float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 4; ++j)
+            d4[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
+            const int64_t n = ncol0 + j;
+            if (n < p.N) drow[n * sn] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(static_cast<uint32_t>(2 * BN)));
+  }
+}
+
 // ---- host: tensor-map encoding through the driver entry point ----
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -484,6 +796,50 @@ int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, cons
   return TNC_OK;
 }
 
+template <int BN, int SWZ, int STAGES, bool F16>
+int launch_cfg_2sm(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, const void* As,
+                   const void* Bb, const void* Bs, const int* ex, const int* ey, void* C, int64_t ldcm,
+                   int64_t ldcn, int k_splits, float* partials, cudaStream_t stream) {
+  using Cfg = Tc2Cfg<BN, SWZ, STAGES, F16>;
+  const int64_t Kr = 2 * Kp;
+  CUtensorMap mAb, mAs, mBb, mBs;
+  TNC_TRY(make_map(&mAb, Ab, M, Kr, kBM, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mAs, As, M, Kr, kBM, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mBb, Bb, 2 * N, Kr, BN / 2, SWZ, Cfg::kElem));
+  TNC_TRY(make_map(&mBs, Bs, 2 * N, Kr, BN / 2, SWZ, Cfg::kElem));
+  TcParams p{};
+  p.M = M;
+  p.N = N;
+  p.num_kb = static_cast<int>(Kr / Cfg::kBK);
+  const int splits = std::max(1, std::min(k_splits, p.num_kb));
+  p.kb_per_split = static_cast<int>(ceil_div(p.num_kb, splits));
+  p.splits = static_cast<int>(ceil_div(p.num_kb, p.kb_per_split));
+  p.m_blocks = static_cast<int>(ceil_div(M, 256));
+  p.n_blocks = static_cast<int>(ceil_div(2 * N, BN));
+  p.group_m = std::max(1, env_int("TNC_GROUP_M", 8));
+  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", 64 / Cfg::kBK));
+  p.C = static_cast<float2*>(C);
+  p.ldcm = ldcm;
+  p.ldcn = ldcn;
+  p.partials = p.splits > 1 ? reinterpret_cast<float2*>(partials) : nullptr;
+  p.ex = ex;
+  p.ey = ey;
+  const int64_t units = static_cast<int64_t>(p.m_blocks) * p.n_blocks * p.splits;
+  if (units > INT32_MAX) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_cgemm: too many tiles");
+  auto kern = tc_cgemm_2sm_kernel<BN, SWZ, STAGES, F16>;
+  TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+  const int pairs = static_cast<int>(std::min<int64_t>(units, num_sms() / 2));
+  {
+    ProfScope prof(PROF_TC_GEMM, 8.0 * M * N * K,
+                   8.0 * (double(M) * K + double(N) * K + double(M) * N), stream);
+    kern<<<2 * pairs, kThreads, Cfg::kSmem, stream>>>(mAb, mAs, mBb, mBs, p);
+    TNC_CHECK_LAUNCH();
+  }
+  if (p.splits > 1)
+    return tree_reduce_launch(TNC_C64, p.splits, M * N, partials, C, M, N, ldcm, ldcn, stream);
+  return TNC_OK;
+}
+
 }  // namespace
 
 int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Abig,
@@ -497,6 +853,7 @@ int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const 
   if (f16) {
     if (2 * N >= 256) {
       if (cfg == 1) return launch_cfg<256, 64, 4, true>(TNC_TC_ARGS);
+      if (cfg == 2 && M >= 256) return launch_cfg_2sm<256, 128, 3, true>(TNC_TC_ARGS);
       return launch_cfg<256, 128, 2, true>(TNC_TC_ARGS);
     }
     return launch_cfg<128, 128, 3, true>(TNC_TC_ARGS);

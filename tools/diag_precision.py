@@ -21,7 +21,7 @@ def tc_err(m, n, k, seed=0, positive=False):
         b = b.real.abs().to(torch.complex64)
     A = DenseTensor([Index("m", m), Index("k", k)], a)
     B = DenseTensor([Index("k", k), Index("n", n)], b)
-    got = contract_pair(A, B, variant=2).data.to(torch.complex128)
+    got = contract_pair(A, B, variant=int(os.environ.get("TNC_VARIANT", "4"))).data.to(torch.complex128)
     simt = contract_pair(A, B, variant=1).data.to(torch.complex128)
     want = a.to(torch.complex128) @ b.to(torch.complex128)
     return ((got - want).norm() / want.norm()).item(), ((simt - want).norm() / want.norm()).item()

@@ -13,7 +13,8 @@ a = torch.randn((M, K), dtype=torch.complex64, device="cuda")
 b = torch.randn((K, N), dtype=torch.complex64, device="cuda")
 A = DenseTensor([Index("m", M), Index("k", K)], a)
 B = DenseTensor([Index("k", K), Index("n", N)], b)
-plan = plan_for(A.indices, a.stride(), B.indices, b.stride(), _lib.C64, None, 2)
+import os
+plan = plan_for(A.indices, a.stride(), B.indices, b.stride(), _lib.C64, None, int(os.environ.get("TNC_VARIANT", "4")))
 out = contract_into(plan, a, b)
 lib = _lib.load()
 torch.cuda.synchronize()
