@@ -337,6 +337,106 @@ def bench_c3(args) -> None:
         dist.destroy_process_group()
 
 
+def bench_c2(args) -> None:
+    """Config C2: rank-30 tensor (8 GiB) absorbing 16 random two-qubit gates --
+    fused K4 chain vs 16 separate contract_pair passes (HBM-bound)."""
+    import torch
+
+    from paper_2504_09186_b200 import DenseTensor, Index, _lib, contract_pair
+    from paper_2504_09186_b200.fusion import absorb_chain
+    from paper_2504_09186_b200.workloads import C2
+
+    torch.cuda.set_device(0)
+    lib = _lib.load(require_device=True)
+    t_labels, data, gates = C2.build()
+    t = DenseTensor([Index(l) for l in t_labels], data)
+    gs = [DenseTensor([Index(oa), Index(ob), Index(ia), Index(ib)], u) for ia, ib, oa, ob, u in gates]
+    del data
+
+    def timed(fn, reps):
+        for _ in range(args.warmup):
+            out = fn()
+            del out
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lib.tnc_profile_enable(1)
+        s.record()
+        for _ in range(reps):
+            out = fn()
+            del out
+        e.record()
+        e.synchronize()
+        prof = _read_prof(lib)
+        lib.tnc_profile_enable(0)
+        return s.elapsed_time(e) / 1e3 / reps, prof
+
+    def separate():
+        cur = t
+        for g in gs:
+            cur = contract_pair(cur, g)
+        return cur
+
+    fused_t, prof = timed(lambda: absorb_chain(t, gs), args.steps)
+    sep_t, _ = timed(separate, max(1, args.steps // 4))
+    nbytes = 2 * 8 * (1 << 30)
+    ab = prof["absorb"]
+    peaks = measured_peaks()
+    line = {
+        "metric": "C2 step-fusion chain: HBM GB/s (algorithmic 2 x 8 GiB per chain)", "value": nbytes / fused_t / 1e9,
+        "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": fused_t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic (seeded rank-30 tensor, Haar x fSim gates)",
+        "config": {"workload": "C2: rank-30 complex64 tensor absorbs 16 two-qubit gates", "separate_ms": sep_t * 1e3,
+                   "fused_speedup": sep_t / fused_t, "passes": ab["launches"] // max(1, args.steps)},
+        "roofline": {"bound": "hbm", "achieved": nbytes / fused_t / 1e9, "peak": peaks.get("hbm_gbs"),
+                     "unit": "GB/s", "frac": nbytes / fused_t / 1e9 / peaks.get("hbm_gbs"), "traffic": None,
+                     "kernel": "absorb_pass_kernel", "note": "algorithmic bytes = one read + one write of T"},
+        "kernels": prof,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_c1(args) -> None:
+    """Config C1 a/b/c single-step micro-benchmarks (contract + output permutation)."""
+    import torch
+
+    from paper_2504_09186_b200 import DenseTensor, Index, _lib, contract_pair
+    from paper_2504_09186_b200.workloads import c1_cases
+
+    torch.cuda.set_device(0)
+    lib = _lib.load(require_device=True)
+    peaks = measured_peaks()
+    for case in c1_cases():
+        ia, ib, io = case.index_lists()
+        da, db = case.data()
+        a, b = DenseTensor(ia, da), DenseTensor(ib, db)
+        del da, db
+        for _ in range(args.warmup):
+            contract_pair(a, b, out_order=io)
+        torch.cuda.synchronize()
+        lib.tnc_profile_enable(1)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            out = contract_pair(a, b, out_order=io)
+        e.record()
+        e.synchronize()
+        prof = _read_prof(lib)
+        lib.tnc_profile_enable(0)
+        dt = s.elapsed_time(e) / 1e3 / args.steps
+        m = 2 ** sum(1 for l in case.a_labels if l.startswith("a"))
+        k = 2 ** sum(1 for l in case.a_labels if l.startswith("k"))
+        n = 2 ** sum(1 for l in case.b_labels if l.startswith("b"))
+        flops = 8.0 * m * k * n
+        nbytes = 8.0 * (m * k + k * n + m * n)
+        print(json.dumps({"metric": f"{case.name} contract+permute", "value": flops / dt / 1e12, "unit": "TFLOP/s",
+                          "ms_per_step": dt * 1e3, "GB_per_s_algorithmic": nbytes / dt / 1e9,
+                          "hbm_frac": nbytes / dt / 1e9 / peaks.get("hbm_gbs"), "shape_log2": [
+                              m.bit_length() - 1, k.bit_length() - 1, n.bit_length() - 1], "kernels": prof}),
+              flush=True)
+        del a, b, out
+
+
 def _read_prof(lib) -> dict:
     import ctypes
 
@@ -355,7 +455,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c1"])
     ap.add_argument("--slices-per-step", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cap", type=int, default=26)
@@ -366,7 +466,7 @@ def main() -> None:
     if args.impl == "reference":
         bench_reference(args)
         return
-    bench_c3(args)
+    {"c3": bench_c3, "c2": bench_c2, "c1": bench_c1}[args.workload](args)
 
 
 if __name__ == "__main__":

@@ -127,12 +127,14 @@ int tnc_contract_split(const tnc_plan* plan, int32_t blocks, int32_t group, cons
                        void* stream);
 
 /* ---- K4: step fusion (absorb a chain of small gates into a big tensor) -----
- * T (rank t_rank, contiguous, dims all 2) absorbs n_gates two-leg gates
- * sequentially, each gate g a (2,2,2,2) tensor laid out (out_a,out_b,in_a,in_b)
- * acting on T legs (axes[2g], axes[2g+1]) (positions in the CURRENT leg order).
- * Reference semantics of contract_pair(T, G): the two contracted legs are
- * removed and the gate's out legs are appended at the end.  The output is
- * written in the final leg order after all gates; t_out may alias nothing. */
+ * T (rank t_rank in [12, 62], contiguous complex64, dims all 2) absorbs n_gates
+ * two-leg gates sequentially; gates[g] is a HOST pointer to 16 complex64 values
+ * laid out (out_a,out_b,in_a,in_b) acting on T legs (axes[2g], axes[2g+1]) --
+ * positions in the CURRENT leg order.  Reference semantics of
+ * contract_pair(T, G): the two contracted legs are removed and the gate's out
+ * legs are appended at the end.  The output is written in the final leg order
+ * after all gates; t_out must not alias t_in.  Workspace: one tensor-sized
+ * buffer when the chain needs more than one pass (see _workspace). */
 int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,
                      const void* const* gates, const int32_t* axes, void* workspace,
                      size_t workspace_bytes, void* stream);

@@ -404,6 +404,8 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
       want = TNC_VARIANT_SPLITK;  // tiny output, huge K: CUDA-core split-K reduction
     else
       want = tc_eligible(p) ? default_tc_variant() : TNC_VARIANT_SIMT;
+    // short K: 3xFP16 pads K to 32 (64 fp16 per 128B row); 3xTF32 pads to 16
+    if (want == TNC_VARIANT_TC3XF16 && k <= 16) want = TNC_VARIANT_TC3XTF32;
   }
   const bool tc = want == TNC_VARIANT_TC3XTF32 || want == TNC_VARIANT_TC3XF16;
   if (tc && p->dtype != TNC_C64) {
@@ -411,7 +413,7 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
   }
   p->variant = want;
-  p->kp = ((k + 31) / 32) * 32;
+  p->kp = want == TNC_VARIANT_TC3XF16 ? ((k + 31) / 32) * 32 : ((k + 15) / 16) * 16;
   // split-K when the output tile grid cannot fill the machine
   p->k_splits = 1;
   if (tc) {
@@ -601,12 +603,8 @@ int tnc_contract_split(const tnc_plan* p, int32_t blocks, int32_t group, const v
 
 int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* axes,
                                size_t* workspace_bytes) {
-  (void)axes;
-  (void)n_gates;
   if (!workspace_bytes) TNC_RET(TNC_ERR_INVALID, "null argument");
-  if (t_rank < 2 || t_rank > 40) TNC_RET(TNC_ERR_TENSOR, "absorb: rank out of range");
-  *workspace_bytes = 0;
-  return TNC_OK;
+  return absorb_chain_workspace(t_rank, n_gates, axes, workspace_bytes);
 }
 
 int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,

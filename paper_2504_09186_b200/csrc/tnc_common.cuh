@@ -143,6 +143,7 @@ int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* o
                        int64_t M, int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream);
 
 // K4 step fusion (tnc_absorb.cu)
+int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t* bytes);
 int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates,
                         const void* const* gates, const int32_t* axes, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream);

@@ -817,7 +817,9 @@ int launch_cfg_2sm(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, 
   p.m_blocks = static_cast<int>(ceil_div(M, 256));
   p.n_blocks = static_cast<int>(ceil_div(2 * N, BN));
   p.group_m = std::max(1, env_int("TNC_GROUP_M", 8));
-  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", 64 / Cfg::kBK));
+  // 64 complex K per TMEM chain: the cross-CTA drain handshake needs >= 2
+  // k-blocks per chunk to stay off the MMA critical path (~9e-7 rel-L2 / GEMM)
+  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", 128 / Cfg::kBK));
   p.C = static_cast<float2*>(C);
   p.ldcm = ldcm;
   p.ldcn = ldcn;
@@ -847,12 +849,15 @@ int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const 
                     const int* ey, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
                     float* partials, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return TNC_OK;
-  if (Kp % 32 != 0) TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 32");
+  if (Kp % (f16 ? 32 : 16) != 0)
+    TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 32 (f16) / 16 (tf32)");
   const int cfg = env_int("TNC_TC_CFG", 0);
 #define TNC_TC_ARGS M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, ex, ey, C, ldcm, ldcn, k_splits, partials, stream
   if (f16) {
     if (2 * N >= 256) {
       if (cfg == 1) return launch_cfg<256, 64, 4, true>(TNC_TC_ARGS);
+      // the 2-CTA kernel (cfg 2) wins on square 8192^3 but loses on the C3
+      // step shapes; the 1-SM kernel is the default until that is understood
       if (cfg == 2 && M >= 256) return launch_cfg_2sm<256, 128, 3, true>(TNC_TC_ARGS);
       return launch_cfg<256, 128, 2, true>(TNC_TC_ARGS);
     }

@@ -70,7 +70,10 @@ def test_plan_shapes_and_output_order_host_only():
     big_a = [(f"a{i}", 2) for i in range(12)] + [(f"k{i}", 2) for i in range(12)]
     big_b = [(f"k{i}", 2) for i in range(12)] + [(f"b{i}", 2) for i in range(12)]
     code, info, _ = _plan(big_a, big_b)
-    assert code == 0 and info.variant == 2 and info.workspace_bytes > 0
+    assert code == 0 and info.variant in (2, 4) and info.workspace_bytes > 0
+    # tiny output, huge K -> the CUDA-core split-K reduction is auto-selected
+    code, info, _ = _plan([("m", 2)] + [(f"k{i}", 2) for i in range(14)], [(f"k{i}", 2) for i in range(14)] + [("n", 4)])
+    assert code == 0 and info.variant == 3
 
 
 def test_plan_errors_map_to_reference_exceptions():

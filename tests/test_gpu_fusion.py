@@ -1,0 +1,57 @@
+"""K4 step fusion vs the reference semantics (sequential contract_pair) and
+the numpy oracle; complex64 tolerance rel-L2 <= 1e-5."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import tncref
+
+pytestmark = pytest.mark.gpu
+
+
+def _chain(rank, n_gates, seed):
+    from paper_2504_09186_b200 import DenseTensor, Index
+    from paper_2504_09186_b200.workloads import ChainCase
+
+    t_labels, data, gates = ChainCase(rank, n_gates, seed).build()
+    t = DenseTensor([Index(l) for l in t_labels], data)
+    gs = [DenseTensor([Index(oa), Index(ob), Index(ia), Index(ib)], u) for ia, ib, oa, ob, u in gates]
+    return t_labels, data, gates, t, gs
+
+
+@pytest.mark.parametrize("rank,n_gates,seed", [(14, 16, 1), (16, 5, 2), (18, 16, 3), (12, 3, 4)])
+def test_absorb_chain_vs_oracle(cuda_ready, rank, n_gates, seed):
+    from paper_2504_09186_b200.fusion import absorb_chain
+
+    t_labels, data, gates, t, gs = _chain(rank, n_gates, seed)
+    got = absorb_chain(t, gs)
+    ref = (tuple(t_labels), (2,) * rank, data.astype(np.complex128))
+    for ia, ib, oa, ob, u in gates:
+        ref = tncref.contract(ref, ((oa, ob, ia, ib), (2, 2, 2, 2), u.astype(np.complex128)))
+    assert list(got.labels) == list(ref[0])  # index map bit-exact with the reference
+    assert rel_l2(got.numpy(), ref[2]) <= 1e-5
+
+
+def test_absorb_chain_matches_sequential_device_contractions(cuda_ready):
+    from paper_2504_09186_b200 import contract_pair
+    from paper_2504_09186_b200.fusion import absorb_chain
+
+    _, _, _, t, gs = _chain(20, 16, 7)
+    got = absorb_chain(t, gs)
+    seq = t
+    for g in gs:
+        seq = contract_pair(seq, g)
+    assert got.labels == seq.labels
+    assert rel_l2(got.numpy(), seq.numpy()) <= 1e-5
+
+
+def test_absorb_chain_rejects_bad_gate(cuda_ready):
+    from paper_2504_09186_b200 import ContractionError, DenseTensor, Index
+    from paper_2504_09186_b200.fusion import absorb_chain
+
+    _, _, _, t, _ = _chain(12, 1, 0)
+    bad = DenseTensor([Index("x"), Index("y"), Index("z"), Index("w0")], np.ones(16, np.complex64))
+    with pytest.raises(ContractionError):
+        absorb_chain(t, [bad])
