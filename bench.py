@@ -129,16 +129,37 @@ def measured_peaks() -> dict:
 # -- workload C3 ---------------------------------------------------------------
 
 
-def plan_c3():
+WORKLOAD_TEXT = {
+    "c3": "C3: 6x6 grid, 14 cycles, seed 0, 64 open amplitudes (q30-35), greedy path seed 0, slices to "
+          "rank<=30 (9 labels, 512 slices)",
+    "c4": "C4: 7x7 grid, 16 cycles, seed 0, 1024 open amplitudes (q39-48), greedy path seed 0, slices to "
+          "rank<=32 (33 labels, 2^33 slices); a fixed seeded subset of 2^10 slice ids is cycled",
+}
+
+
+def plan_workload(name: str = "c3"):
+    """Reference path (greedy seed 0) + reference slicing; returns
+    (workload, network, tree, schedule, spec, multiplies per slice, slice ids)."""
+    import numpy as np
+
     from paper_2504_09186_b200 import greedy_path, linearize, select_slices, tree_metrics
     from paper_2504_09186_b200 import workloads
 
-    wl = workloads.C3
+    wl, cap = (workloads.C3, workloads.C3_MAX_RANK) if name == "c3" else (workloads.C4, workloads.C4_MAX_RANK)
     net = wl.network()
     t = greedy_path(net, 0)
-    spec = select_slices(t, workloads.C3_MAX_RANK, 64, 0)
+    spec = select_slices(t, cap, 64, 0)
     s = linearize(t)
     per_slice = tree_metrics(t, spec.dims_projected()).total_cost
+    if spec.n_subtasks <= 4096:
+        ids = list(range(spec.n_subtasks))
+    else:
+        ids = sorted(int(x) for x in np.random.default_rng(0).choice(spec.n_subtasks, 1024, replace=False))
+    return wl, net, t, s, spec, per_slice, ids
+
+
+def plan_c3():
+    wl, net, t, s, spec, per_slice, _ = plan_workload("c3")
     return wl, net, t, s, spec, per_slice
 
 
@@ -212,16 +233,16 @@ def bench_c3(args) -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load(require_device=True)
-    wl, net, t, s, spec, per_slice = plan_c3()
+    wl, net, t, s, spec, per_slice, slice_ids = plan_workload(args.workload)
     order = wl.output_order()
     ex = SliceExecutor(net, s, spec, "single", order)
     ex.prepare()
-    n_slices = spec.n_subtasks
+    n_ids = len(slice_ids)
     spp = args.slices_per_step
 
     def ids_for(step: int):
         base = (step * world + rank) * spp
-        return [(base + j) % n_slices for j in range(spp)]
+        return [slice_ids[(base + j) % n_ids] for j in range(spp)]
 
     acc = None
     for i in range(args.warmup):
@@ -274,7 +295,7 @@ def bench_c3(args) -> None:
         for i in range(args.e2e_steps):
             dev = [DenseTensor.__new__(DenseTensor)._init_raw(tt_.indices, hl.to("cuda", non_blocking=True))
                    for tt_, hl in zip(net.tensors, host_leaves)]
-            amps = run_open(TensorNetwork(dev), t, spec, order, "single", slice_ids=[i]).data.cpu()
+            amps = run_open(TensorNetwork(dev), t, spec, order, "single", slice_ids=[slice_ids[i % n_ids]]).data.cpu()
             d2h = amps.numel() * amps.element_size()
         e_e.record()
         torch.cuda.synchronize()
@@ -311,15 +332,16 @@ def bench_c3(args) -> None:
             mult = tree_metrics(t, sub.dims_projected()).total_cost
             secs = run_cpu_subslice(net, s, sub, 0)
             cpu = {"value": 8 * mult / secs / 1e12, "unit": "TFLOP/s", "cores": _threads(), "kind": "port",
-                   "sample": f"one C3 sub-slice (extra slicing to rank {args.cpu_cap}: {len(sub.entries)} labels, "
+                   "sample": f"one {args.workload.upper()} sub-slice (extra slicing to rank {args.cpu_cap}: {len(sub.entries)} labels, "
                              f"{mult} multiplies) through the numpy oracle of tncsim's step loop, {secs:.1f}s"}
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-            "data": "synthetic (seeded 6x6 grid random circuit, SURVEY Appendix A)",
-            "config": {"workload": "C3: 6x6 grid, 14 cycles, seed 0, 64 open amplitudes (q30-35), greedy path "
-                                   "seed 0, slices to rank<=30 (9 labels, 512 slices)",
+            "data": "synthetic (seeded grid random circuit, SURVEY Appendix A)",
+            "config": {"workload": WORKLOAD_TEXT[args.workload],
+                       "total_slices": spec.n_subtasks,
+                       "extrapolated_hours_all_slices_this_job": spec.n_subtasks / (slices_total / elapsed) / 3600,
                        "slices_per_step_per_gpu": spp, "slices_per_s": slices_total / elapsed,
                        "flops_per_slice": 8 * per_slice, "l2": "inputs > L2 (intermediates up to 8 GiB)",
                        "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce"},
@@ -455,7 +477,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c1"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c2", "c1"])
     ap.add_argument("--slices-per-step", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cap", type=int, default=26)
@@ -466,7 +488,7 @@ def main() -> None:
     if args.impl == "reference":
         bench_reference(args)
         return
-    {"c3": bench_c3, "c2": bench_c2, "c1": bench_c1}[args.workload](args)
+    {"c3": bench_c3, "c4": bench_c3, "c2": bench_c2, "c1": bench_c1}[args.workload](args)
 
 
 if __name__ == "__main__":

@@ -442,7 +442,8 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     const size_t pe = p->variant == TNC_VARIANT_TC3XF16 ? 2 : 4;
     const size_t a_plane = align_up(static_cast<size_t>(p->rows_x) * 2 * p->kp * pe);
     const size_t b_plane = align_up(static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * pe);
-    off = align_up(off + 2 * a_plane + 2 * b_plane + align_up(4 * p->rows_x) + 4 * p->rows_y);
+    off = align_up(off + 2 * a_plane + 2 * b_plane + align_up(4 * p->rows_x) + align_up(4 * p->rows_y) +
+                   4 * std::max(p->rows_x, p->rows_y));
   }
   p->off_partials = off;
   if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
@@ -508,8 +509,9 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     int* ex = reinterpret_cast<int*>(bs + b_plane);
     int* ey = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ex) + align_up(4 * p->rows_x));
     if (f16) {
-      TNC_TRY(f16_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, ex, st));
-      TNC_TRY(f16_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, ey, st));
+      void* scratch = reinterpret_cast<uint8_t*>(ey) + align_up(4 * p->rows_y);
+      TNC_TRY(f16_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, ex, scratch, st));
+      TNC_TRY(f16_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, ey, scratch, st));
     } else {
       TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
       TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));

@@ -28,18 +28,24 @@ namespace {
 constexpr int kTileBits = 12;              // 4096 complex64 = 32 KB tile
 constexpr int kTile = 1 << kTileBits;
 constexpr int kMaxSectionGates = 16;
-constexpr int kThreadsAbs = 512;
+constexpr int kThreadsAbs = 256;           // one 16-element gate-group item per thread
 
+// Gates of a section are applied in groups whose legs span <= 4 tile bits: a
+// thread keeps the 16-element sub-cube in registers and applies every gate of
+// the group before writing it back (2 shared-memory round trips per group
+// instead of 2 per gate).
 struct AbsorbParams {
   int n_outer;
-  int n_gates;
+  int n_groups;
   int64_t n_tiles;
   // 2-level tables over the tile index (low 6 bits / high 6 bits)
   int64_t in_lo[64], in_hi[64];    // input element offset of load index e
   int64_t out_lo[64], out_hi[64];  // output element offset of store index f
   int src_lo[64], src_hi[64];      // load index e holding store index f
-  int gate_bits[kMaxSectionGates][2];  // tile bit of in_a, in_b (load enumeration)
-  float2 u[kMaxSectionGates][16];      // U[(oa,ob),(ia,ib)] row-major
+  int group_bits[kMaxSectionGates][4];  // ascending tile bits of the group's sub-cube
+  int group_gates[kMaxSectionGates][2]; // [first gate, last gate) of the group
+  int gate_local[kMaxSectionGates];     // 4 * (local bit of in_a) + local bit of in_b
+  float2 u[kMaxSectionGates][16];       // U[(oa,ob),(ia,ib)] row-major
   int outer_shift[TNC_MAX_RANK];       // outer axis digit = (t >> shift) & 1
   int64_t outer_in[TNC_MAX_RANK];
   int64_t outer_out[TNC_MAX_RANK];
@@ -53,20 +59,84 @@ __device__ __forceinline__ float2 cmul_add(float2 acc, float2 a, float2 b) {
   return acc;
 }
 
+// 4x4 gate on local bits (LA = in_a, LB = in_b) of a 16-element register cube
+template <int LA, int LB>
+__device__ __forceinline__ void apply_local(float2 (&v)[16], const float2* __restrict__ u) {
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    if ((s >> LA) & 1) continue;
+    if ((s >> LB) & 1) continue;
+    const int i1 = s | (1 << LB), i2 = s | (1 << LA), i3 = s | (1 << LA) | (1 << LB);
+    const float2 x0 = v[s], x1 = v[i1], x2 = v[i2], x3 = v[i3];
+    float2 y[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      float2 acc = make_float2(0.f, 0.f);
+      acc = cmul_add(acc, u[o * 4 + 0], x0);
+      acc = cmul_add(acc, u[o * 4 + 1], x1);
+      acc = cmul_add(acc, u[o * 4 + 2], x2);
+      acc = cmul_add(acc, u[o * 4 + 3], x3);
+      y[o] = acc;
+    }
+    v[s] = y[0];
+    v[i1] = y[1];
+    v[i2] = y[2];
+    v[i3] = y[3];
+  }
+}
+
+__device__ __forceinline__ void apply_gate(float2 (&v)[16], int local, const float2* __restrict__ u) {
+  switch (local) {
+    case 1: apply_local<0, 1>(v, u); break;
+    case 2: apply_local<0, 2>(v, u); break;
+    case 3: apply_local<0, 3>(v, u); break;
+    case 4: apply_local<1, 0>(v, u); break;
+    case 6: apply_local<1, 2>(v, u); break;
+    case 7: apply_local<1, 3>(v, u); break;
+    case 8: apply_local<2, 0>(v, u); break;
+    case 9: apply_local<2, 1>(v, u); break;
+    case 11: apply_local<2, 3>(v, u); break;
+    case 12: apply_local<3, 0>(v, u); break;
+    case 13: apply_local<3, 1>(v, u); break;
+    case 14: apply_local<3, 2>(v, u); break;
+    default: break;
+  }
+}
+
 __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* __restrict__ in,
                                                                   float2* __restrict__ out,
                                                                   const AbsorbParams p) {
   __shared__ float2 tile[kTile];
   __shared__ int64_t s_base[2];
+  // per-element table lookups must not hit the (serialising) param/constant
+  // bank with divergent addresses: stage the tables in shared memory
+  __shared__ int64_t t_in_lo[64], t_in_hi[64], t_out_lo[64], t_out_hi[64];
+  __shared__ int t_src_lo[64], t_src_hi[64];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  __shared__ int64_t s_oin[TNC_MAX_RANK], s_oout[TNC_MAX_RANK];
+  __shared__ int s_oshift[TNC_MAX_RANK];
+  if (tid < p.n_outer) {
+    s_oin[tid] = p.outer_in[tid];
+    s_oout[tid] = p.outer_out[tid];
+    s_oshift[tid] = p.outer_shift[tid];
+  }
+  if (tid < 64) {
+    t_in_lo[tid] = p.in_lo[tid];
+    t_in_hi[tid] = p.in_hi[tid];
+    t_out_lo[tid] = p.out_lo[tid];
+    t_out_hi[tid] = p.out_hi[tid];
+    t_src_lo[tid] = p.src_lo[tid];
+    t_src_hi[tid] = p.src_hi[tid];
+  }
+  __syncthreads();
   for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
     if (tid < 32) {
       int64_t bi = 0, bo = 0;
       for (int a = lane; a < p.n_outer; a += 32) {
-        const int64_t d = (t >> p.outer_shift[a]) & 1;
-        bi += d * p.outer_in[a];
-        bo += d * p.outer_out[a];
+        const int64_t d = (t >> s_oshift[a]) & 1;
+        bi += d * s_oin[a];
+        bo += d * s_oout[a];
       }
 #pragma unroll
       for (int s = 16; s > 0; s >>= 1) {
@@ -86,42 +156,43 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = tid + i * kThreadsAbs;
-      v[i] = src[p.in_lo[e & 63] + p.in_hi[e >> 6]];
+      v[i] = src[t_in_lo[e & 63] + t_in_hi[e >> 6]];
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) tile[tid + i * kThreadsAbs] = v[i];
     __syncthreads();
-    for (int g = 0; g < p.n_gates; ++g) {
-      const int ba = p.gate_bits[g][0], bb = p.gate_bits[g][1];
-      const int lo = min(ba, bb), hi = max(ba, bb);
-      // quartets: insert zero bits at positions lo and hi into q
-      for (int q = tid; q < kTile / 4; q += kThreadsAbs) {
+    for (int g = 0; g < p.n_groups; ++g) {
+      const int b0 = p.group_bits[g][0], b1 = p.group_bits[g][1];
+      const int b2 = p.group_bits[g][2], b3 = p.group_bits[g][3];
+      for (int q = tid; q < kTile / 16; q += kThreadsAbs) {
+        // insert zero bits at b0 < b1 < b2 < b3 into the 8-bit cube index q
         int base = q;
-        base = ((base >> lo) << (lo + 1)) | (base & ((1 << lo) - 1));
-        base = ((base >> hi) << (hi + 1)) | (base & ((1 << hi) - 1));
-        const int ia[4] = {base, base | (1 << bb), base | (1 << ba), base | (1 << ba) | (1 << bb)};
-        float2 x[4];
+        base = ((base >> b0) << (b0 + 1)) | (base & ((1 << b0) - 1));
+        base = ((base >> b1) << (b1 + 1)) | (base & ((1 << b1) - 1));
+        base = ((base >> b2) << (b2 + 1)) | (base & ((1 << b2) - 1));
+        base = ((base >> b3) << (b3 + 1)) | (base & ((1 << b3) - 1));
+        float2 c[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = tile[ia[j]];
+        for (int s = 0; s < 16; ++s)
+          c[s] = tile[base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
+                      (((s >> 3) & 1) << b3)];
+        for (int k = p.group_gates[g][0]; k < p.group_gates[g][1]; ++k) apply_gate(c, p.gate_local[k], p.u[k]);
 #pragma unroll
-        for (int o = 0; o < 4; ++o) {
-          float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc = cmul_add(acc, p.u[g][o * 4 + j], x[j]);
-          tile[ia[o]] = acc;
-        }
+        for (int s = 0; s < 16; ++s)
+          tile[base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
+               (((s >> 3) & 1) << b3)] = c[s];
       }
       __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int f = tid + i * kThreadsAbs;
-      v[i] = tile[p.src_lo[f & 63] | p.src_hi[f >> 6]];
+      v[i] = tile[t_src_lo[f & 63] | t_src_hi[f >> 6]];
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int f = tid + i * kThreadsAbs;
-      dst[p.out_lo[f & 63] + p.out_hi[f >> 6]] = v[i];
+      dst[t_out_lo[f & 63] + t_out_hi[f >> 6]] = v[i];
     }
     __syncthreads();
   }
@@ -225,13 +296,42 @@ int launch_pass(int r, const Section& sec, const std::vector<GateRef>& gates, co
     p.src_lo[i] = slo;
     p.src_hi[i] = shi;
   }
-  p.n_gates = static_cast<int>(sec.gates.size());
-  for (int g = 0; g < p.n_gates; ++g) {
-    const GateRef& gr = gates[sec.gates[g]];
-    p.gate_bits[g][0] = bit_of[gr.pa];
-    p.gate_bits[g][1] = bit_of[gr.pb];
-    std::memcpy(p.u[g], gr.u, 16 * sizeof(float2));  // host gate data baked into the launch
+  // group consecutive gates whose legs span <= 4 tile bits
+  const int n_gates = static_cast<int>(sec.gates.size());
+  std::vector<int> cur_bits;
+  p.n_groups = 0;
+  auto close_group = [&](int end) {
+    if (cur_bits.empty()) return;
+    std::vector<int> bits = cur_bits;
+    for (int b = 0; static_cast<int>(bits.size()) < 4; ++b)
+      if (std::find(bits.begin(), bits.end(), b) == bits.end()) bits.push_back(b);
+    std::sort(bits.begin(), bits.end());
+    const int g = p.n_groups;
+    for (int i = 0; i < 4; ++i) p.group_bits[g][i] = bits[i];
+    p.group_gates[g][1] = end;
+    for (int k = p.group_gates[g][0]; k < end; ++k) {
+      const GateRef& gr = gates[sec.gates[k]];
+      const int la = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pa]) - bits.begin());
+      const int lb = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pb]) - bits.begin());
+      p.gate_local[k] = 4 * la + lb;
+    }
+    ++p.n_groups;
+    cur_bits.clear();
+  };
+  for (int k = 0; k < n_gates; ++k) {
+    const GateRef& gr = gates[sec.gates[k]];
+    std::memcpy(p.u[k], gr.u, 16 * sizeof(float2));  // host gate data baked into the launch
+    std::vector<int> trial = cur_bits;
+    for (int b : {bit_of[gr.pa], bit_of[gr.pb]})
+      if (std::find(trial.begin(), trial.end(), b) == trial.end()) trial.push_back(b);
+    if (trial.size() > 4) {
+      close_group(k);
+      trial = {bit_of[gr.pa], bit_of[gr.pb]};
+    }
+    if (cur_bits.empty()) p.group_gates[p.n_groups][0] = k;
+    cur_bits = trial;
   }
+  close_group(n_gates);
   // outer axes: physical axes not in the tile, enumerated least significant first
   std::vector<int> outer;
   for (int a = r - 1; a >= 0; --a)
@@ -244,7 +344,7 @@ int launch_pass(int r, const Section& sec, const std::vector<GateRef>& gates, co
   }
   p.n_tiles = static_cast<int64_t>(1) << p.n_outer;
   const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()) * 4);
-  ProfScope prof(PROF_ABSORB, 32.0 * p.n_gates * (static_cast<double>(1) * (int64_t(1) << r)),
+  ProfScope prof(PROF_ABSORB, 32.0 * n_gates * (static_cast<double>(1) * (int64_t(1) << r)),
                  16.0 * static_cast<double>(int64_t(1) << r), stream);
   absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreadsAbs, 0, stream>>>(in, out, p);
   TNC_CHECK_LAUNCH();

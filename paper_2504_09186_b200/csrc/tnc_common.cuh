@@ -130,7 +130,8 @@ int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X,
 // 3xFP16 prep: per-row power-of-two scaled hi/lo fp16 planes (same shapes as
 // tf32_split_launch, 2-byte elements) + per-row scale exponents
 int f16_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
-                     void* hi, void* lo, int* exps, cudaStream_t stream);
+                     void* hi, void* lo, int* exps, void* scratch /* 4*R bytes */,
+                     cudaStream_t stream);
 // tcgen05 complex GEMM on prepared planes (see tnc_gemm_tc.cu).  f16 = 0:
 // 3xTF32 fp32 planes; f16 = 1: 3xFP16 half planes with row/column scale
 // exponents ex (rows of A) / ey (complex columns of C).

@@ -347,6 +347,61 @@ __global__ void __launch_bounds__(256) f16_split_kernel(int mode, int64_t R, int
   }
 }
 
+// Few, very long rows (e.g. the (7,20,7) split-K step): phase 1 reduces each
+// row's max |component| across many blocks (non-negative floats order like
+// their bit patterns, so atomicMax on the bits is exact), phase 2 splits
+// element-parallel.
+__global__ void row_absmax_kernel(int64_t R, int64_t K, const c64* __restrict__ X, int64_t ldx,
+                                  unsigned* __restrict__ rowmax) {
+  const int64_t r = blockIdx.y;
+  float mx = 0.f;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    c64 v = X[r * ldx + k];
+    mx = fmaxf(mx, fmaxf(fabsf(v.re), fabsf(v.im)));
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  if ((threadIdx.x & 31) == 0) atomicMax(rowmax + r, __float_as_uint(mx));
+}
+
+__global__ void f16_split_elem_kernel(int mode, int64_t R, int64_t K, int64_t Kp,
+                                      const c64* __restrict__ X, int64_t ldx, __half* __restrict__ hi,
+                                      __half* __restrict__ lo, const unsigned* __restrict__ rowmax,
+                                      int* __restrict__ exps) {
+  const int64_t total = R * Kp;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / Kp;
+    const int64_t k = e - r * Kp;
+    const float mx = __uint_as_float(rowmax[r]);
+    int ex = 0;
+    if (mx > 0.f && isfinite(mx)) frexpf(mx, &ex);
+    if (k == 0) exps[r] = ex;
+    const float sc = ldexpf(1.f, -ex);
+    float re = 0.f, im = 0.f;
+    if (k < K) {
+      c64 v = X[r * ldx + k];
+      re = v.re * sc;
+      im = v.im * sc;
+    }
+    const __half hre = __float2half_rn(re), him = __float2half_rn(im);
+    const __half lre = __float2half_rn(re - __half2float(hre));
+    const __half lim = __float2half_rn(im - __half2float(him));
+    if (mode == 0) {
+      reinterpret_cast<__half2*>(hi)[r * Kp + k] = __halves2half2(hre, him);
+      reinterpret_cast<__half2*>(lo)[r * Kp + k] = __halves2half2(lre, lim);
+    } else {
+      __half2* h0 = reinterpret_cast<__half2*>(hi) + (2 * r) * Kp + k;
+      __half2* l0 = reinterpret_cast<__half2*>(lo) + (2 * r) * Kp + k;
+      h0[0] = __halves2half2(hre, __hneg(him));
+      l0[0] = __halves2half2(lre, __hneg(lim));
+      h0[Kp] = __halves2half2(him, hre);
+      l0[Kp] = __halves2half2(lim, lre);
+    }
+  }
+}
+
 // Fixed-order pairwise tree over P partial tiles [P][MN] (complex, fp32 or
 // fp64): level by level, partial i += partial i+stride, exactly the
 // left-complete combine of contract.py:200-207.  The root is written to
@@ -483,9 +538,25 @@ int tf32_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X,
 }
 
 int f16_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, int64_t ldx,
-                     void* hi, void* lo, int* exps, cudaStream_t stream) {
+                     void* hi, void* lo, int* exps, void* scratch, cudaStream_t stream) {
   if (R <= 0 || Kp <= 0) return TNC_OK;
   ProfScope prof(PROF_SPLIT_PREP, 0.0, 8.0 * R * K + (mode ? 16.0 : 8.0) * R * Kp, stream);
+  if (R < static_cast<int64_t>(num_sms()) * 32 && K >= 4096 && R <= 65535) {
+    // few long rows: cross-block row max (into `scratch`), then an
+    // element-parallel split that derives the scale exponents
+    unsigned* rowmax = static_cast<unsigned*>(scratch);
+    TNC_CUDA_TRY(cudaMemsetAsync(rowmax, 0, static_cast<size_t>(R) * sizeof(unsigned), stream));
+    const int64_t per_row = std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, 256 * 8),
+                                                                   num_sms() * 8 / std::max<int64_t>(R, 1) + 1));
+    row_absmax_kernel<<<dim3(static_cast<unsigned>(per_row), static_cast<unsigned>(R)), 256, 0, stream>>>(
+        R, K, static_cast<const c64*>(X), ldx, rowmax);
+    TNC_CHECK_LAUNCH();
+    f16_split_elem_kernel<<<grid_for(R * Kp), 256, 0, stream>>>(mode, R, K, Kp, static_cast<const c64*>(X), ldx,
+                                                               static_cast<__half*>(hi), static_cast<__half*>(lo),
+                                                               rowmax, exps);
+    TNC_CHECK_LAUNCH();
+    return TNC_OK;
+  }
   const int64_t blocks = std::min<int64_t>(ceil_div(R, 8), static_cast<int64_t>(num_sms()) * 16);
   f16_split_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(
       mode, R, K, Kp, static_cast<const c64*>(X), ldx, static_cast<__half*>(hi), static_cast<__half*>(lo),

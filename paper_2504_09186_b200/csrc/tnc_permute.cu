@@ -70,6 +70,19 @@ __device__ __forceinline__ void warp_decode(int64_t id, const OuterAxes& o, int 
   bout = so;
 }
 
+// The decode indexes the axis tables per lane; from the kernel-parameter bank
+// those divergent loads serialise, so each block stages them in smem first.
+__device__ __forceinline__ void stage_outer(const OuterAxes& src, OuterAxes& dst) {
+  if (threadIdx.x == 0) dst.n = src.n;
+  for (int a = threadIdx.x; a < src.n; a += blockDim.x) {
+    dst.dim[a] = src.dim[a];
+    dst.div[a] = src.div[a];
+    dst.sin[a] = src.sin[a];
+    dst.sout[a] = src.sout[a];
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int pad_idx(int e) { return e + (e >> 4); }
 
 constexpr int kTileThreads = 256;
@@ -129,10 +142,12 @@ __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __r
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  __shared__ OuterAxes so;
+  stage_outer(p.outer, so);
   for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
     if (tid < 32) {
       int64_t bin, bout;
-      warp_decode(t, p.outer, lane, bin, bout);
+      warp_decode(t, so, lane, bin, bout);
       if (lane == 0) {
         s_base[0] = bin;
         s_base[1] = bout;
@@ -176,9 +191,11 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const T* __restrict__
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  __shared__ OuterAxes so;
+  stage_outer(p.outer, so);
   for (int64_t r = warp; r < p.n_rows; r += n_warps) {
     int64_t bin, bout;
-    warp_decode(r, p.outer, lane, bin, bout);
+    warp_decode(r, so, lane, bin, bout);
     const T* src = in + bin;
     T* dst = out + bout;
     int64_t i = lane;
