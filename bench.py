@@ -1,7 +1,11 @@
 """Benchmark of the B200 TNC hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3|c1a|c1b|c1c] [--slices-per-step S]
+                    [--workload c3|c4|c2|c1] [--slices-per-step S]
+
+(c4: the 7x7x16 circuit, rank-32 slices over a seeded 2^10 subset of the 2^33
+slice ids; c2: the fused absorb chain vs 16 separate passes; c1: the three
+single-step micro-benchmarks.  Only c3 is the driver's bench line.)
 
 Default workload (config C3 of BASELINE.json, the largest single-GPU one the
 metric "TNC effective TFLOP/s & slices/s" is quoted on): 6x6 grid random

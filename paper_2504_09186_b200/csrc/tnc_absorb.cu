@@ -51,6 +51,12 @@ struct AbsorbParams {
   int64_t outer_out[TNC_MAX_RANK];
 };
 
+// XOR swizzle of the smem tile: 8-byte elements, 16 per 128-byte bank row.
+// Gate-group accesses step the tile index by powers of two; folding bits
+// 4..11 into the low nibble spreads those strides over the 16 bank slots
+// (ncu: ~75% of shared wavefronts were bank conflicts without it).
+__device__ __forceinline__ int swz(int e) { return e ^ (((e >> 4) ^ (e >> 8)) & 15); }
+
 __device__ __forceinline__ float2 cmul_add(float2 acc, float2 a, float2 b) {
   acc.x = fmaf(a.x, b.x, acc.x);
   acc.x = fmaf(-a.y, b.y, acc.x);
@@ -103,11 +109,21 @@ __device__ __forceinline__ void apply_gate(float2 (&v)[16], int local, const flo
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gmem_src)
+               : "memory");
+}
+
+// Double-buffered pass: tile t+1 streams into the second smem buffer
+// (cp.async) while the gates of tile t run, so HBM time and FP32 gate math
+// overlap instead of alternating.
 __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* __restrict__ in,
                                                                   float2* __restrict__ out,
                                                                   const AbsorbParams p) {
-  __shared__ float2 tile[kTile];
-  __shared__ int64_t s_base[2];
+  extern __shared__ __align__(16) float2 tiles[];  // 2 x kTile
+  __shared__ int64_t s_base[2][2];
   // per-element table lookups must not hit the (serialising) param/constant
   // bank with divergent addresses: stage the tables in shared memory
   __shared__ int64_t t_in_lo[64], t_in_hi[64], t_out_lo[64], t_out_hi[64];
@@ -130,7 +146,8 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
     t_src_hi[tid] = p.src_hi[tid];
   }
   __syncthreads();
-  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+  constexpr int kPer = kTile / kThreadsAbs;
+  auto decode = [&](int64_t t, int slot) {
     if (tid < 32) {
       int64_t bi = 0, bo = 0;
       for (int a = lane; a < p.n_outer; a += 32) {
@@ -144,23 +161,38 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
         bo += __shfl_xor_sync(0xffffffffu, bo, s);
       }
       if (lane == 0) {
-        s_base[0] = bi;
-        s_base[1] = bo;
+        s_base[slot][0] = bi;
+        s_base[slot][1] = bo;
       }
     }
-    __syncthreads();
-    const float2* src = in + s_base[0];
-    float2* dst = out + s_base[1];
-    constexpr int kPer = kTile / kThreadsAbs;
-    float2 v[kPer];
+  };
+  auto issue_loads = [&](int slot) {
+    const float2* src = in + s_base[slot][0];
+    float2* dstt = tiles + slot * kTile;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = tid + i * kThreadsAbs;
-      v[i] = src[t_in_lo[e & 63] + t_in_hi[e >> 6]];
+      cp_async8(dstt + swz(e), src + t_in_lo[e & 63] + t_in_hi[e >> 6]);
     }
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) tile[tid + i * kThreadsAbs] = v[i];
+  };
+  int slot = 0;
+  if (blockIdx.x < p.n_tiles) {
+    decode(blockIdx.x, 0);
     __syncthreads();
+    issue_loads(0);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, slot ^= 1) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < p.n_tiles) decode(tn, slot ^ 1);
+    __syncthreads();  // next base visible; previous store phase done with slot ^ 1
+    if (tn < p.n_tiles) issue_loads(slot ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();  // tile t resident
+    float2* tile = tiles + slot * kTile;
+    float2* dst = out + s_base[slot][1];
+    float2 v[kPer];
     for (int g = 0; g < p.n_groups; ++g) {
       const int b0 = p.group_bits[g][0], b1 = p.group_bits[g][1];
       const int b2 = p.group_bits[g][2], b3 = p.group_bits[g][3];
@@ -174,28 +206,28 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
         float2 c[16];
 #pragma unroll
         for (int s = 0; s < 16; ++s)
-          c[s] = tile[base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
-                      (((s >> 3) & 1) << b3)];
+          c[s] = tile[swz(base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
+                          (((s >> 3) & 1) << b3))];
         for (int k = p.group_gates[g][0]; k < p.group_gates[g][1]; ++k) apply_gate(c, p.gate_local[k], p.u[k]);
 #pragma unroll
         for (int s = 0; s < 16; ++s)
-          tile[base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
-               (((s >> 3) & 1) << b3)] = c[s];
+          tile[swz(base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
+                   (((s >> 3) & 1) << b3))] = c[s];
       }
       __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int f = tid + i * kThreadsAbs;
-      v[i] = tile[t_src_lo[f & 63] | t_src_hi[f >> 6]];
+      v[i] = tile[swz(t_src_lo[f & 63] | t_src_hi[f >> 6])];
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int f = tid + i * kThreadsAbs;
       dst[t_out_lo[f & 63] + t_out_hi[f >> 6]] = v[i];
     }
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 struct GateRef {
@@ -346,7 +378,10 @@ int launch_pass(int r, const Section& sec, const std::vector<GateRef>& gates, co
   const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()) * 4);
   ProfScope prof(PROF_ABSORB, 32.0 * n_gates * (static_cast<double>(1) * (int64_t(1) << r)),
                  16.0 * static_cast<double>(int64_t(1) << r), stream);
-  absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreadsAbs, 0, stream>>>(in, out, p);
+  const size_t smem = 2 * kTile * sizeof(float2);
+  TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+  absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreadsAbs, smem, stream>>>(in, out, p);
   TNC_CHECK_LAUNCH();
   return TNC_OK;
 }
