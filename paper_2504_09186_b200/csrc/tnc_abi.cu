@@ -107,6 +107,19 @@ struct tnc_plan {
   size_t off_x, off_y, off_planes, off_partials, off_tmp, ws_bytes;
   int32_t k_splits;
   __int128 multiplies;
+  // split-K with in-kernel gather (no operand permutation): packed offset
+  // tables [rowx | rowy | tx0 tx1 tx2 | ty0 ty1 ty2], uploaded once per plan
+  bool gather_splitk = false;
+  int32_t g_levels = 0;
+  int64_t g_size[3] = {1, 1, 1};
+  int32_t g_x_kfast = 1, g_y_kfast = 1;
+  int64_t g_chunks = 1;
+  std::vector<int64_t> g_host;
+  mutable std::mutex g_mu;
+  mutable int64_t* g_dev = nullptr;
+  ~tnc_plan() {
+    if (g_dev) cudaFree(g_dev);
+  }
 };
 
 namespace tnc {
@@ -178,6 +191,79 @@ void build_gather(Operand& op) {
     op.strides.push_back(l.stride);
     op.perm.push_back(idx++);
   }
+}
+
+// Offsets of every row of a leg group (first leg most significant).
+void group_offsets(const std::vector<Leg>& legs, std::vector<int64_t>& out) {
+  out.assign(1, 0);
+  for (const Leg& l : legs) {
+    std::vector<int64_t> next;
+    next.reserve(out.size() * l.dim);
+    for (int64_t base : out)
+      for (int64_t d = 0; d < l.dim; ++d) next.push_back(base + d * l.stride);
+    out.swap(next);
+  }
+}
+
+// Split-K with the operand gathers folded into the kernel: rows of X / Y are
+// small tables, the common legs (X's memory order) are cut into <= 3 levels of
+// <= 1024 entries so a K index decodes to 3 table lookups per operand.
+bool build_gather_splitk(tnc_plan* p) {
+  const Operand& X = p->x;
+  const Operand& Y = p->y;
+  if (p->rows_x > 64 || p->rows_y > 64 || X.common.empty()) return false;
+  const int nc = static_cast<int>(X.common.size());
+  std::vector<std::vector<int>> levels;
+  int i = nc - 1;
+  while (i >= 0 && levels.size() < 3) {
+    std::vector<int> idx;
+    int64_t prod = 1;
+    while (i >= 0 && prod * X.common[i].dim <= 1024) {
+      idx.insert(idx.begin(), i);
+      prod *= X.common[i].dim;
+      --i;
+    }
+    if (idx.empty()) return false;
+    levels.push_back(idx);
+  }
+  if (i >= 0) return false;
+  std::vector<int64_t> rowx, rowy;
+  group_offsets(X.free, rowx);
+  group_offsets(Y.free, rowy);
+  std::vector<int64_t> tx[3], ty[3];
+  for (size_t l = 0; l < levels.size(); ++l) {
+    std::vector<Leg> lx, ly;
+    for (int j : levels[l]) {
+      lx.push_back(X.common[j]);
+      ly.push_back(Y.common[j]);
+    }
+    group_offsets(lx, tx[l]);
+    group_offsets(ly, ty[l]);
+    p->g_size[l] = static_cast<int64_t>(tx[l].size());
+  }
+  p->g_levels = static_cast<int32_t>(levels.size());
+  for (size_t l = levels.size(); l < 3; ++l) {
+    tx[l].assign(1, 0);
+    ty[l].assign(1, 0);
+    p->g_size[l] = 1;
+  }
+  auto min_free = [](const Operand& o) {
+    int64_t s = INT64_MAX;
+    for (const Leg& l : o.free)
+      if (l.dim > 1) s = std::min(s, l.stride);
+    return s;
+  };
+  p->g_x_kfast = X.common.back().stride < min_free(X) ? 1 : 0;
+  p->g_y_kfast = Y.common.back().stride < min_free(Y) ? 1 : 0;
+  p->g_host.clear();
+  for (auto* v : {&rowx, &rowy, &tx[0], &tx[1], &tx[2], &ty[0], &ty[1], &ty[2]})
+    p->g_host.insert(p->g_host.end(), v->begin(), v->end());
+  const int64_t target = static_cast<int64_t>(num_sms()) * 4;
+  int64_t kc = ceil_div(p->k, target);
+  kc = std::max<int64_t>(64, ceil_div(kc, 64) * 64);
+  p->g_chunks = ceil_div(p->k, kc);
+  p->gather_splitk = true;
+  return true;
 }
 
 // 3xFP16 (2x-rate kind::f16, half the operand bytes) unless TNC_TC_TF32=1
@@ -413,6 +499,9 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
   }
   p->variant = want;
+  if (want == TNC_VARIANT_SPLITK && build_gather_splitk(p)) {
+    X.in_place = Y.in_place = true;  // the kernel gathers from the original strides
+  }
   p->kp = want == TNC_VARIANT_TC3XF16 ? ((k + 31) / 32) * 32 : ((k + 15) / 16) * 16;
   // split-K when the output tile grid cannot fill the machine
   p->k_splits = 1;
@@ -447,8 +536,10 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   p->off_partials = off;
   if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
-  if (p->variant == TNC_VARIANT_SPLITK)
-    off = align_up(off + static_cast<size_t>(splitk_chunks(p->rows_x, p->rows_y, k)) * m * n * eb);
+  if (p->variant == TNC_VARIANT_SPLITK) {
+    const int64_t chunks = p->gather_splitk ? p->g_chunks : splitk_chunks(p->rows_x, p->rows_y, k);
+    off = align_up(off + static_cast<size_t>(chunks) * m * n * eb);
+  }
   p->off_tmp = off;
   if (p->custom_out) off = align_up(off + static_cast<size_t>(m) * n * eb);
   p->ws_bytes = off;
@@ -519,6 +610,19 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     return tc_cgemm_launch(f16 ? 1 : 0, p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs,
                            f16 ? ex : nullptr, f16 ? ey : nullptr, c, ldcm, ldcn, k_splits,
                            reinterpret_cast<float*>(ws + p->off_partials), st);
+  }
+  if (p->variant == TNC_VARIANT_SPLITK && p->gather_splitk) {
+    {
+      std::lock_guard<std::mutex> lk(p->g_mu);
+      if (!p->g_dev) {
+        const size_t bytes = p->g_host.size() * sizeof(int64_t);
+        TNC_CUDA_TRY(cudaMalloc(&p->g_dev, bytes));
+        TNC_CUDA_TRY(cudaMemcpy(p->g_dev, p->g_host.data(), bytes, cudaMemcpyHostToDevice));
+      }
+    }
+    return splitk_gather_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ym, p->g_dev, p->g_size,
+                                p->g_x_kfast, p->g_y_kfast, p->g_chunks, c, ldcm, ldcn,
+                                ws + p->off_partials, st);
   }
   if (p->variant == TNC_VARIANT_SPLITK)
     return simt_splitk_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ldx, ym, ldy, c, ldcm, ldcn,

@@ -119,6 +119,12 @@ int64_t splitk_chunks(int64_t M, int64_t N, int64_t K);
 int simt_splitk_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, int64_t ldx,
                        const void* Y, int64_t ldy, void* C, int64_t ldcm, int64_t ldcn, void* parts,
                        cudaStream_t stream);
+// split-K with in-kernel operand gathers: `tabs` = device [rowx(M) | rowy(N) |
+// tx0 tx1 tx2 | ty0 ty1 ty2] (level sizes `lvl`), K index k = k0 + s0*(k1 + s1*k2)
+int splitk_gather_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, const void* Y,
+                         const int64_t* tabs, const int64_t* lvl, int x_kfast, int y_kfast,
+                         int64_t chunks, void* C, int64_t ldcm, int64_t ldcn, void* parts,
+                         cudaStream_t stream);
 // axpy y += x
 int axpy_launch(int dtype, int64_t n, const void* x, void* y, cudaStream_t stream);
 // 3xTF32 prep: split complex X[R, K] (row-major, K contiguous, leading dim ldx)

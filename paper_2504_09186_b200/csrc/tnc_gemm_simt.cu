@@ -237,6 +237,117 @@ __global__ void __launch_bounds__(256) simt_splitk_kernel(int64_t M, int64_t N, 
   }
 }
 
+// Split-K with in-kernel gathers (K3 for the tiny-output, huge-K steps such as
+// C4's (6,26,4) closing contraction): no operand permutation pass.  Block b
+// folds K range [b*kc, ...) in chunks of 64: the X rows (<= 64) and Y rows
+// (<= 64) of the chunk are gathered straight from the strided operands into
+// shared memory -- walking K contiguously when the operand's innermost leg is
+// a common leg, rows contiguously otherwise -- and every thread accumulates
+// up to 16 of the M*N outputs.  Partials [block][M][N] go to the fixed-order
+// tree reduction.
+template <typename T>
+__global__ void __launch_bounds__(256) splitk_gather_kernel(
+    int64_t M, int64_t N, int64_t K, int64_t kc, const T* __restrict__ X, const T* __restrict__ Y,
+    const int64_t* __restrict__ tabs, int64_t s0, int64_t s1, int64_t s2, int x_kfast, int y_kfast,
+    T* __restrict__ parts) {
+  using R = typename real_of<T>::type;
+  constexpr int CK = 64;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xs = reinterpret_cast<T*>(smem_raw);      // [M][CK + 1]
+  T* ys = xs + M * (CK + 1);                    // [N][CK + 1]
+  const int64_t* rowx = tabs;
+  const int64_t* rowy = rowx + M;
+  const int64_t* tx0 = rowy + N;
+  const int64_t* tx1 = tx0 + s0;
+  const int64_t* tx2 = tx1 + s1;
+  const int64_t* ty0 = tx2 + s2;
+  const int64_t* ty1 = ty0 + s0;
+  const int64_t* ty2 = ty1 + s1;
+  const int64_t k_lo = static_cast<int64_t>(blockIdx.x) * kc;
+  const int64_t k_hi = min(K, k_lo + kc);
+  const int tid = threadIdx.x;
+  const int n_out = static_cast<int>(M * N);
+  // qubit legs make the level sizes powers of two: decode with shifts, not
+  // 64-bit divisions (which dominated the gather cost)
+  const bool pow2 = ((s0 & (s0 - 1)) == 0) && ((s1 & (s1 - 1)) == 0);
+  const int sh0 = __ffsll(s0) - 1, sh1 = __ffsll(s1) - 1;
+  auto decode = [&](int64_t k, int64_t& a, int64_t& b, int64_t& c) {
+    if (pow2) {
+      a = k & (s0 - 1);
+      b = (k >> sh0) & (s1 - 1);
+      c = k >> (sh0 + sh1);
+    } else {
+      a = k % s0;
+      const int64_t q = k / s0;
+      b = q % s1;
+      c = q / s1;
+    }
+  };
+  R acc_re[16], acc_im[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc_re[j] = acc_im[j] = R(0);
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += CK) {
+    for (int e = tid; e < M * CK; e += 256) {
+      int m, kk;
+      if (x_kfast) { m = e / CK; kk = e % CK; } else { m = e % static_cast<int>(M); kk = e / static_cast<int>(M); }
+      const int64_t k = k0 + kk;
+      T v;
+      if (k < k_hi) {
+        int64_t a, b, c;
+        decode(k, a, b, c);
+        v = X[rowx[m] + tx0[a] + tx1[b] + tx2[c]];
+      } else {
+        v.re = v.im = R(0);
+      }
+      xs[m * (CK + 1) + kk] = v;
+    }
+    for (int e = tid; e < N * CK; e += 256) {
+      int n, kk;
+      if (y_kfast) { n = e / CK; kk = e % CK; } else { n = e % static_cast<int>(N); kk = e / static_cast<int>(N); }
+      const int64_t k = k0 + kk;
+      T v;
+      if (k < k_hi) {
+        int64_t a, b, c;
+        decode(k, a, b, c);
+        v = Y[rowy[n] + ty0[a] + ty1[b] + ty2[c]];
+      } else {
+        v.re = v.im = R(0);
+      }
+      ys[n * (CK + 1) + kk] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int o = tid + j * 256;
+      if (o >= n_out) break;
+      const int m = o / static_cast<int>(N), n = o % static_cast<int>(N);
+      const T* xr = xs + m * (CK + 1);
+      const T* yr = ys + n * (CK + 1);
+      R re = acc_re[j], im = acc_im[j];
+#pragma unroll 8
+      for (int kk = 0; kk < CK; ++kk) {
+        const T a = xr[kk], b = yr[kk];
+        re = fma(a.re, b.re, re);
+        re = fma(-a.im, b.im, re);
+        im = fma(a.re, b.im, im);
+        im = fma(a.im, b.re, im);
+      }
+      acc_re[j] = re;
+      acc_im[j] = im;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int o = tid + j * 256;
+    if (o >= n_out) break;
+    T v;
+    v.re = acc_re[j];
+    v.im = acc_im[j];
+    parts[static_cast<int64_t>(blockIdx.x) * n_out + o] = v;
+  }
+}
+
 template <typename T>
 __global__ void axpy_kernel(int64_t n, const T* __restrict__ x, T* __restrict__ y) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -509,6 +620,36 @@ int simt_splitk_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X
       simt_splitk_kernel<c64, 4, 8><<<grid, 256, 0, stream>>>(M, N, K, kc, static_cast<const c64*>(X), ldx,
                                                               static_cast<const c64*>(Y), ldy,
                                                               static_cast<c64*>(parts));
+    TNC_CHECK_LAUNCH();
+  }
+  return tree_reduce_launch(dtype, chunks, M * N, parts, C, M, N, ldcm, ldcn, stream);
+}
+
+int splitk_gather_launch(int dtype, int64_t M, int64_t N, int64_t K, const void* X, const void* Y,
+                         const int64_t* tabs, const int64_t* lvl, int x_kfast, int y_kfast,
+                         int64_t chunks, void* C, int64_t ldcm, int64_t ldcn, void* parts,
+                         cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return TNC_OK;
+  if (M > 64 || N > 64 || M * N > 4096) TNC_RET(TNC_ERR_UNSUPPORTED, "gather split-K: output too large");
+  const int64_t kc = ceil_div(K, chunks);
+  const size_t eb = elem_bytes(dtype);
+  const size_t smem = static_cast<size_t>(M + N) * 65 * eb;
+  {
+    ProfScope prof(PROF_SIMT_GEMM, 8.0 * M * N * K, double(eb) * (double(M) * K + double(N) * K + double(M) * N),
+                   stream);
+    if (dtype == TNC_C128) {
+      auto k = splitk_gather_kernel<c128>;
+      TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<static_cast<unsigned>(chunks), 256, smem, stream>>>(M, N, K, kc, static_cast<const c128*>(X),
+                                                              static_cast<const c128*>(Y), tabs, lvl[0], lvl[1],
+                                                              lvl[2], x_kfast, y_kfast, static_cast<c128*>(parts));
+    } else {
+      auto k = splitk_gather_kernel<c64>;
+      TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<static_cast<unsigned>(chunks), 256, smem, stream>>>(M, N, K, kc, static_cast<const c64*>(X),
+                                                              static_cast<const c64*>(Y), tabs, lvl[0], lvl[1],
+                                                              lvl[2], x_kfast, y_kfast, static_cast<c64*>(parts));
+    }
     TNC_CHECK_LAUNCH();
   }
   return tree_reduce_launch(dtype, chunks, M * N, parts, C, M, N, ldcm, ldcn, stream);

@@ -12,7 +12,8 @@ from paper_2504_09186_b200.contract import plan_for
 from paper_2504_09186_b200.execute import SliceExecutor
 
 top = int(sys.argv[1]) if len(sys.argv) > 1 else 25
-wl, net, t, s, spec, per = bench.plan_c3()
+work = sys.argv[2] if len(sys.argv) > 2 else "c3"
+wl, net, t, s, spec, per, _ids = bench.plan_workload(work)
 ex = SliceExecutor(net, s, spec, "single", wl.output_order())
 ex.prepare()
 ex.run_slice(spec.assignment(0))  # warm plans
