@@ -283,6 +283,15 @@ __global__ void __launch_bounds__(256) splitk_gather_kernel(
       c = q / s1;
     }
   };
+  // compute mapping: 4x4 output blocks, `ksplit` threads per block taking
+  // interleaved k (consecutive threads -> consecutive k: conflict-free smem)
+  const int nbm = static_cast<int>((M + 3) / 4), nbn = static_cast<int>((N + 3) / 4);
+  const int nblk = nbm * nbn;
+  int ksplit = 1;
+  while (ksplit * 2 * nblk <= 256) ksplit *= 2;
+  const int g = tid % ksplit, blk = tid / ksplit;
+  const bool active = blk < nblk;
+  const int m0 = active ? (blk / nbn) * 4 : 0, n0 = active ? (blk % nbn) * 4 : 0;
   R acc_re[16], acc_im[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc_re[j] = acc_im[j] = R(0);
@@ -316,34 +325,54 @@ __global__ void __launch_bounds__(256) splitk_gather_kernel(
       ys[n * (CK + 1) + kk] = v;
     }
     __syncthreads();
+    if (active) {
+      for (int kk = g; kk < CK; kk += ksplit) {
+        T a[4], b[4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int o = tid + j * 256;
-      if (o >= n_out) break;
-      const int m = o / static_cast<int>(N), n = o % static_cast<int>(N);
-      const T* xr = xs + m * (CK + 1);
-      const T* yr = ys + n * (CK + 1);
-      R re = acc_re[j], im = acc_im[j];
-#pragma unroll 8
-      for (int kk = 0; kk < CK; ++kk) {
-        const T a = xr[kk], b = yr[kk];
-        re = fma(a.re, b.re, re);
-        re = fma(-a.im, b.im, re);
-        im = fma(a.re, b.im, im);
-        im = fma(a.im, b.re, im);
+        for (int i = 0; i < 4; ++i) {
+          const int m = min(m0 + i, static_cast<int>(M) - 1);
+          const int n = min(n0 + i, static_cast<int>(N) - 1);
+          a[i] = xs[m * (CK + 1) + kk];
+          b[i] = ys[n * (CK + 1) + kk];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            R re = acc_re[4 * i + j], im = acc_im[4 * i + j];
+            re = fma(a[i].re, b[j].re, re);
+            re = fma(-a[i].im, b[j].im, re);
+            im = fma(a[i].re, b[j].im, im);
+            im = fma(a[i].im, b[j].re, im);
+            acc_re[4 * i + j] = re;
+            acc_im[4 * i + j] = im;
+          }
       }
-      acc_re[j] = re;
-      acc_im[j] = im;
     }
     __syncthreads();
   }
+  // fixed-order reduction over the k-groups of each output block
+  R* red = reinterpret_cast<R*>(smem_raw);  // [256 threads][32]
+  if (active) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int o = tid + j * 256;
-    if (o >= n_out) break;
+    for (int j = 0; j < 16; ++j) {
+      red[tid * 32 + 2 * j] = acc_re[j];
+      red[tid * 32 + 2 * j + 1] = acc_im[j];
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < n_out; o += 256) {
+    const int m = o / static_cast<int>(N), n = o % static_cast<int>(N);
+    const int b = (m / 4) * nbn + n / 4;
+    const int j = (m % 4) * 4 + (n % 4);
+    R re = R(0), im = R(0);
+    for (int gg = 0; gg < ksplit; ++gg) {
+      re += red[(b * ksplit + gg) * 32 + 2 * j];
+      im += red[(b * ksplit + gg) * 32 + 2 * j + 1];
+    }
     T v;
-    v.re = acc_re[j];
-    v.im = acc_im[j];
+    v.re = re;
+    v.im = im;
     parts[static_cast<int64_t>(blockIdx.x) * n_out + o] = v;
   }
 }
@@ -633,7 +662,8 @@ int splitk_gather_launch(int dtype, int64_t M, int64_t N, int64_t K, const void*
   if (M > 64 || N > 64 || M * N > 4096) TNC_RET(TNC_ERR_UNSUPPORTED, "gather split-K: output too large");
   const int64_t kc = ceil_div(K, chunks);
   const size_t eb = elem_bytes(dtype);
-  const size_t smem = static_cast<size_t>(M + N) * 65 * eb;
+  // operand tiles, reused afterwards for the k-group reduction (256 x 16 complex)
+  const size_t smem = std::max(static_cast<size_t>(M + N) * 65 * eb, static_cast<size_t>(256) * 16 * eb);
   {
     ProfScope prof(PROF_SIMT_GEMM, 8.0 * M * N * K, double(eb) * (double(M) * K + double(N) * K + double(M) * N),
                    stream);
