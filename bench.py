@@ -467,7 +467,7 @@ def _read_prof(lib) -> dict:
     import ctypes
 
     out = {}
-    for kind, name in enumerate(["tc_gemm", "simt_gemm", "permute", "split_prep", "reduce", "absorb", "axpy"]):
+    for kind, name in enumerate(["tc_gemm", "simt_gemm", "permute", "split_prep", "reduce", "absorb", "axpy", "stream"]):
         n = ctypes.c_int64()
         ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         lib.tnc_profile_read(kind, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by))

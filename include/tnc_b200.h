@@ -65,8 +65,11 @@ typedef enum tnc_variant {
   TNC_VARIANT_SIMT = 1,        /* CUDA-core complex GEMM (fp32 / fp64 accumulate) */
   TNC_VARIANT_TC3XTF32 = 2,    /* tcgen05 kind::tf32, 3xTF32 split, TMEM accum    */
   TNC_VARIANT_SPLITK = 3,      /* CUDA-core split-K, fixed-order tree (tiny M*N)  */
-  TNC_VARIANT_TC3XF16 = 4      /* tcgen05 kind::f16, 2-piece FP16 split with
+  TNC_VARIANT_TC3XF16 = 4,     /* tcgen05 kind::f16, 2-piece FP16 split with
                                   per-row power-of-two scaling, TMEM accum        */
+  TNC_VARIANT_STREAM = 5       /* narrow step: X streamed once in place, small Y
+                                  on chip, C written in the final order (c64,
+                                  extent-2 legs, rows_y * K <= 4096)              */
 } tnc_variant;
 
 /* A labeled operand: leg i has label id labels[i], extent dims[i], element
@@ -151,7 +154,7 @@ int tnc_axpy(int32_t dtype, int64_t n, const void* x, void* y, void* stream);
  * launching stream; tnc_profile_read sums launches / device ms / algorithmic
  * flops / algorithmic bytes for one kernel kind:
  *   0 tensor-core GEMM, 1 CUDA-core GEMM, 2 permute, 3 3xTF32 operand prep,
- *   4 split-K reduce, 5 absorb chain, 6 axpy. */
+ *   4 split-K reduce, 5 absorb chain, 6 axpy, 7 streaming contraction. */
 int64_t tnc_launch_count(void);
 int tnc_profile_enable(int on);
 int tnc_profile_read(int32_t kind, int64_t* launches, double* total_ms, double* flops,

@@ -105,6 +105,8 @@ struct tnc_plan {
   std::vector<int64_t> out_dims;
   // workspace layout (bytes)
   size_t off_x, off_y, off_planes, off_partials, off_tmp, ws_bytes;
+  size_t ws_layout;  // bytes of the staged-operand layout (split path); == ws_bytes unless streaming
+  tnc::StreamPlan* stream = nullptr;  // TNC_VARIANT_STREAM
   int32_t k_splits;
   __int128 multiplies;
   // split-K with in-kernel gather (no operand permutation): packed offset
@@ -119,6 +121,7 @@ struct tnc_plan {
   mutable int64_t* g_dev = nullptr;
   ~tnc_plan() {
     if (g_dev) cudaFree(g_dev);
+    if (stream) tnc::stream_destroy(stream);
   }
 };
 
@@ -270,6 +273,45 @@ bool build_gather_splitk(tnc_plan* p) {
 int default_tc_variant() {
   const char* v = std::getenv("TNC_TC_TF32");
   return (v && std::atoi(v) != 0) ? TNC_VARIANT_TC3XTF32 : TNC_VARIANT_TC3XF16;
+}
+
+// K5 streaming path: every leg of extent 2 (extent-1 legs are dropped), a
+// small Y (rows_y * K <= 4096) and a large X.  Builds the kernel tables with
+// the FINAL output strides, so the result needs no separate permutation.
+int try_stream(tnc_plan* p, const std::vector<Leg>& free_a, const std::vector<Leg>& free_b) {
+  if (p->dtype != TNC_C64) return TNC_ERR_UNSUPPORTED;
+  const Operand& X = p->x;
+  const Operand& Y = p->y;
+  for (const auto* v : {&X.free, &X.common, &Y.free, &Y.common})
+    for (const Leg& l : *v)
+      if (l.dim != 1 && l.dim != 2) return TNC_ERR_UNSUPPORTED;
+  if (p->rows_y * p->k > 4096) return TNC_ERR_UNSUPPORTED;
+  // final output strides by label
+  std::vector<Leg> order;
+  if (p->custom_out) {
+    std::vector<Leg> def_out = free_a;
+    def_out.insert(def_out.end(), free_b.begin(), free_b.end());
+    for (int32_t i : p->out_perm) order.push_back(def_out[i]);
+  } else {
+    order = free_a;
+    order.insert(order.end(), free_b.begin(), free_b.end());
+  }
+  auto out_stride = [&](int32_t label) {
+    int64_t s = 1;
+    for (int i = static_cast<int>(order.size()) - 1; i >= 0; --i) {
+      if (order[i].label == label) return s;
+      s *= order[i].dim;
+    }
+    return static_cast<int64_t>(-1);
+  };
+  std::vector<StreamLeg> legs;
+  for (const Leg& l : X.free)
+    if (l.dim == 2) legs.push_back({0, l.stride, 0, out_stride(l.label)});
+  for (size_t i = 0; i < X.common.size(); ++i)
+    if (X.common[i].dim == 2) legs.push_back({1, X.common[i].stride, Y.common[i].stride, 0});
+  for (const Leg& l : Y.free)
+    if (l.dim == 2) legs.push_back({2, 0, l.stride, out_stride(l.label)});
+  return stream_prepare(static_cast<int>(legs.size()), legs.data(), &p->stream);
 }
 
 bool tc_eligible(const tnc_plan* p) {
@@ -498,6 +540,16 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     delete p;
     TNC_RET(TNC_ERR_UNSUPPORTED, "tensor-core variant needs complex64");
   }
+  if (want == TNC_VARIANT_STREAM || (variant == TNC_VARIANT_AUTO && want != TNC_VARIANT_SPLITK &&
+                                       p->rows_x >= 4096 && (p->rows_y <= 16 || !tc_eligible(p)))) {
+    const int st = try_stream(p, free_a, free_b);
+    if (st == TNC_OK) {
+      want = TNC_VARIANT_STREAM;
+    } else if (want == TNC_VARIANT_STREAM) {
+      delete p;
+      return st;
+    }
+  }
   p->variant = want;
   if (want == TNC_VARIANT_SPLITK && build_gather_splitk(p)) {
     X.in_place = Y.in_place = true;  // the kernel gathers from the original strides
@@ -543,6 +595,8 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   p->off_tmp = off;
   if (p->custom_out) off = align_up(off + static_cast<size_t>(m) * n * eb);
   p->ws_bytes = off;
+  p->ws_layout = off;
+  if (want == TNC_VARIANT_STREAM) p->ws_bytes = 0;  // reads A/B in place, writes C in final order
   *plan_out = p;
   return TNC_OK;
 }
@@ -639,6 +693,7 @@ int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void*
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const void* xsrc = p->x_is_a ? a : b;
   const void* ysrc = p->x_is_a ? b : a;
+  if (p->variant == TNC_VARIANT_STREAM) return stream_launch(p->stream, xsrc, ysrc, c, st);
   const void *xm, *ym;
   int64_t ldx, ldy;
   TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
@@ -659,7 +714,7 @@ int tnc_contract_split_workspace(const tnc_plan* p, int32_t blocks, int32_t grou
   if (blocks < 1 || group < 1) TNC_RET(TNC_ERR_CONTRACTION, "blocks*group_size must be positive");
   const int64_t panels = std::min<int64_t>(static_cast<int64_t>(blocks) * group, p->k);
   const size_t eb = elem_bytes(p->dtype);
-  size_t need = align_up(p->ws_bytes) + align_up(static_cast<size_t>(panels) * p->m * p->n * eb);
+  size_t need = align_up(p->ws_layout) + align_up(static_cast<size_t>(panels) * p->m * p->n * eb);
   // operand gathers are always materialised for the split path
   need += align_up(static_cast<size_t>(p->rows_x) * p->k * eb) +
           align_up(static_cast<size_t>(p->rows_y) * p->k * eb);
@@ -677,7 +732,7 @@ int tnc_contract_split(const tnc_plan* p, int32_t blocks, int32_t group, const v
   const int64_t panels = std::min<int64_t>(static_cast<int64_t>(blocks) * group, p->k);
   const int64_t base = p->k / panels;
   const size_t eb = elem_bytes(p->dtype);
-  uint8_t* parts = ws + align_up(p->ws_bytes);
+  uint8_t* parts = ws + align_up(p->ws_layout);
   const void* xsrc = p->x_is_a ? a : b;
   const void* ysrc = p->x_is_a ? b : a;
   const void *xm, *ym;

@@ -16,6 +16,7 @@
 // so a 16-gate chain on a rank-30 tensor costs ~4 passes instead of 16
 // permute+GEMM round trips.  Index maps are 2-level bit tables (all dims 2).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -28,10 +29,13 @@ namespace {
 constexpr int kTileBits = 12;              // 4096 complex64 = 32 KB tile
 constexpr int kTile = 1 << kTileBits;
 constexpr int kMaxSectionGates = 16;
-constexpr int kThreadsAbs = 256;           // one 16-element gate-group item per thread
+constexpr int kCubeBits = 5;               // register cube: 32 complex per thread
+constexpr int kCube = 1 << kCubeBits;
+constexpr int kThreadBits = kTileBits - kCubeBits;
+constexpr int kThreadsAbs = 1 << kThreadBits;  // one cube per thread in the gate phase
 
-// Gates of a section are applied in groups whose legs span <= 4 tile bits: a
-// thread keeps the 16-element sub-cube in registers and applies every gate of
+// Gates of a section are applied in groups whose legs span <= 5 tile bits: a
+// thread keeps the 32-element sub-cube in registers and applies every gate of
 // the group before writing it back (2 shared-memory round trips per group
 // instead of 2 per gate).
 struct AbsorbParams {
@@ -41,12 +45,15 @@ struct AbsorbParams {
   // 2-level tables over the tile index (low 6 bits / high 6 bits)
   int64_t in_lo[64], in_hi[64];    // input element offset of load index e
   int64_t out_lo[64], out_hi[64];  // output element offset of store index f
-  int src_lo[64], src_hi[64];      // load index e holding store index f
-  int group_bits[kMaxSectionGates][4];  // ascending tile bits of the group's sub-cube
-  int group_gates[kMaxSectionGates][2]; // [first gate, last gate) of the group
-  int gate_local[kMaxSectionGates];     // 4 * (local bit of in_a) + local bit of in_b
-  float2 u[kMaxSectionGates][16];       // U[(oa,ob),(ia,ib)] row-major
-  int outer_shift[TNC_MAX_RANK];       // outer axis digit = (t >> shift) & 1
+  int src_lo[64], src_hi[64];      // swizzled smem slot of store index f (XOR halves)
+  // swizzled smem slot of each sub-cube bit (register index bit j) and of each
+  // thread-index bit (cube base) of a group; all other slots are XORs of these
+  int group_cube[kMaxSectionGates][kCubeBits];
+  int group_lane[kMaxSectionGates][kThreadBits];
+  int group_gates[kMaxSectionGates][2];         // [first gate, last gate) of the group
+  int gate_local[kMaxSectionGates];             // 8 * (local bit of in_a) + local bit of in_b, a < b
+  float4 u[kMaxSectionGates][16];  // U[(oa,ob),(ia,ib)] row-major as (re, im, -im, re)
+  int outer_shift[TNC_MAX_RANK];   // outer axis digit = (t >> shift) & 1
   int64_t outer_in[TNC_MAX_RANK];
   int64_t outer_out[TNC_MAX_RANK];
 };
@@ -54,99 +61,131 @@ struct AbsorbParams {
 // XOR swizzle of the smem tile: 8-byte elements, 16 per 128-byte bank row.
 // Gate-group accesses step the tile index by powers of two; folding bits
 // 4..11 into the low nibble spreads those strides over the 16 bank slots
-// (ncu: ~75% of shared wavefronts were bank conflicts without it).
-__device__ __forceinline__ int swz(int e) { return e ^ (((e >> 4) ^ (e >> 8)) & 15); }
+// (ncu: ~75% of shared wavefronts were bank conflicts without it).  swz is
+// linear over GF(2): swz(x ^ y) = swz(x) ^ swz(y), so a cube's 32 slots are
+// one per-thread base XOR a per-group pattern.
+__host__ __device__ __forceinline__ int swz(int e) { return e ^ (((e >> 4) ^ (e >> 8)) & 15); }
 
-__device__ __forceinline__ float2 cmul_add(float2 acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, acc.x);
-  acc.x = fmaf(-a.y, b.y, acc.x);
-  acc.y = fmaf(a.x, b.y, acc.y);
-  acc.y = fmaf(a.y, b.x, acc.y);
-  return acc;
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 as_u64(float2 v) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 as_f2(u64 r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ u64 bcast(float x) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+// packed fp32x2 FMA (sm_100 FFMA2): one issue slot for both halves
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
 }
 
-// 4x4 gate on local bits (LA = in_a, LB = in_b) of a 16-element register cube
+// acc += u * x as two FFMA2: (x.re, x.re) * (u.re, u.im) + (x.im, x.im) * (-u.im, u.re)
+__device__ __forceinline__ u64 cmac(u64 acc, float4 u, float2 x) {
+  acc = ffma2(bcast(x.x), as_u64(make_float2(u.x, u.y)), acc);
+  return ffma2(bcast(x.y), as_u64(make_float2(u.z, u.w)), acc);
+}
+
+// 4x4 gate on local bits (LA = in_a < LB = in_b) of a 32-element register cube
 template <int LA, int LB>
-__device__ __forceinline__ void apply_local(float2 (&v)[16], const float2* __restrict__ u) {
+__device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* __restrict__ u) {
 #pragma unroll
-  for (int s = 0; s < 16; ++s) {
+  for (int s = 0; s < kCube; ++s) {
     if ((s >> LA) & 1) continue;
     if ((s >> LB) & 1) continue;
     const int i1 = s | (1 << LB), i2 = s | (1 << LA), i3 = s | (1 << LA) | (1 << LB);
     const float2 x0 = v[s], x1 = v[i1], x2 = v[i2], x3 = v[i3];
-    float2 y[4];
+    u64 y[4];
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
-      float2 acc = make_float2(0.f, 0.f);
-      acc = cmul_add(acc, u[o * 4 + 0], x0);
-      acc = cmul_add(acc, u[o * 4 + 1], x1);
-      acc = cmul_add(acc, u[o * 4 + 2], x2);
-      acc = cmul_add(acc, u[o * 4 + 3], x3);
+      u64 acc = 0;
+      acc = cmac(acc, u[o * 4 + 0], x0);
+      acc = cmac(acc, u[o * 4 + 1], x1);
+      acc = cmac(acc, u[o * 4 + 2], x2);
+      acc = cmac(acc, u[o * 4 + 3], x3);
       y[o] = acc;
     }
-    v[s] = y[0];
-    v[i1] = y[1];
-    v[i2] = y[2];
-    v[i3] = y[3];
+    v[s] = as_f2(y[0]);
+    v[i1] = as_f2(y[1]);
+    v[i2] = as_f2(y[2]);
+    v[i3] = as_f2(y[3]);
   }
 }
 
-__device__ __forceinline__ void apply_gate(float2 (&v)[16], int local, const float2* __restrict__ u) {
+// The host orients every gate so that its in_a bit is the lower local bit
+// (U transposed accordingly), leaving 10 (a < b) cases.
+__device__ __forceinline__ void apply_gate(float2 (&v)[kCube], int local, const float4* __restrict__ u) {
   switch (local) {
-    case 1: apply_local<0, 1>(v, u); break;
-    case 2: apply_local<0, 2>(v, u); break;
-    case 3: apply_local<0, 3>(v, u); break;
-    case 4: apply_local<1, 0>(v, u); break;
-    case 6: apply_local<1, 2>(v, u); break;
-    case 7: apply_local<1, 3>(v, u); break;
-    case 8: apply_local<2, 0>(v, u); break;
-    case 9: apply_local<2, 1>(v, u); break;
-    case 11: apply_local<2, 3>(v, u); break;
-    case 12: apply_local<3, 0>(v, u); break;
-    case 13: apply_local<3, 1>(v, u); break;
-    case 14: apply_local<3, 2>(v, u); break;
+    case 8 * 0 + 1: apply_local<0, 1>(v, u); break;
+    case 8 * 0 + 2: apply_local<0, 2>(v, u); break;
+    case 8 * 0 + 3: apply_local<0, 3>(v, u); break;
+    case 8 * 0 + 4: apply_local<0, 4>(v, u); break;
+    case 8 * 1 + 2: apply_local<1, 2>(v, u); break;
+    case 8 * 1 + 3: apply_local<1, 3>(v, u); break;
+    case 8 * 1 + 4: apply_local<1, 4>(v, u); break;
+    case 8 * 2 + 3: apply_local<2, 3>(v, u); break;
+    case 8 * 2 + 4: apply_local<2, 4>(v, u); break;
+    case 8 * 3 + 4: apply_local<3, 4>(v, u); break;
     default: break;
   }
 }
 
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src)
-               : "memory");
+__device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_dst), "l"(gmem_src) : "memory");
 }
 
-// Double-buffered pass: tile t+1 streams into the second smem buffer
-// (cp.async) while the gates of tile t run, so HBM time and FP32 gate math
-// overlap instead of alternating.
+// One pass: tiles of 2^12 elements stream HBM -> smem (cp.async, coalesced
+// along the input-fastest axes), the section's gates run on 32-element
+// register cubes (one per thread, FFMA2), and the tile leaves smem in the
+// output order.  NBUF = 2 overlaps the next tile's loads with this tile's
+// gates inside the block; NBUF = 1 relies on co-resident blocks for that.
+template <int NBUF>
 __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* __restrict__ in,
                                                                   float2* __restrict__ out,
                                                                   const AbsorbParams p) {
-  extern __shared__ __align__(16) float2 tiles[];  // 2 x kTile
-  __shared__ int64_t s_base[2][2];
+  extern __shared__ __align__(16) float2 tiles[];  // NBUF x kTile
+  // tile bases ring-indexed by iteration: a fast warp decoding tile i+1 can
+  // never overwrite a base a slow warp still reads (it passed iteration i's barrier)
+  __shared__ int64_t s_base[4][2];
   // per-element table lookups must not hit the (serialising) param/constant
   // bank with divergent addresses: stage the tables in shared memory
-  __shared__ int64_t t_in_lo[64], t_in_hi[64], t_out_lo[64], t_out_hi[64];
-  __shared__ int t_src_lo[64], t_src_hi[64];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  __shared__ int64_t t_in_hi[64], t_out_hi[64];
+  __shared__ int t_src_hi[64];
   __shared__ int64_t s_oin[TNC_MAX_RANK], s_oout[TNC_MAX_RANK];
   __shared__ int s_oshift[TNC_MAX_RANK];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
   if (tid < p.n_outer) {
     s_oin[tid] = p.outer_in[tid];
     s_oout[tid] = p.outer_out[tid];
     s_oshift[tid] = p.outer_shift[tid];
   }
   if (tid < 64) {
-    t_in_lo[tid] = p.in_lo[tid];
     t_in_hi[tid] = p.in_hi[tid];
-    t_out_lo[tid] = p.out_lo[tid];
     t_out_hi[tid] = p.out_hi[tid];
-    t_src_lo[tid] = p.src_lo[tid];
     t_src_hi[tid] = p.src_hi[tid];
   }
+  // element e = tid + kThreadsAbs * i: its low 6 bits are the thread's own
+  // (kThreadsAbs is a multiple of 64), its high 6 bits are (tid >> 6) + 2 i
+  const int64_t my_in_lo = p.in_lo[tid & 63];
+  const int my_swz = swz(tid);
+  const int64_t my_out_lo = p.out_lo[tid & 63];
+  const int my_src_lo = p.src_lo[tid & 63];
+  const int hi0 = tid >> 6;
+  const uint32_t tiles_s = static_cast<uint32_t>(__cvta_generic_to_shared(tiles));
   __syncthreads();
   constexpr int kPer = kTile / kThreadsAbs;
+  static_assert(kPer == kCube, "one cube per thread");
   auto decode = [&](int64_t t, int slot) {
     if (tid < 32) {
       int64_t bi = 0, bo = 0;
@@ -166,68 +205,75 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
       }
     }
   };
-  auto issue_loads = [&](int slot) {
-    const float2* src = in + s_base[slot][0];
-    float2* dstt = tiles + slot * kTile;
+  auto issue_loads = [&](int slot, int bslot) {
+    const float2* src = in + s_base[bslot][0] + my_in_lo;
+    const uint32_t dst = tiles_s + slot * kTile * 8;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int e = tid + i * kThreadsAbs;
-      cp_async8(dstt + swz(e), src + t_in_lo[e & 63] + t_in_hi[e >> 6]);
-    }
+    for (int i = 0; i < kPer; ++i)
+      cp_async8(dst + ((my_swz ^ swz(kThreadsAbs * i)) << 3), src + t_in_hi[hi0 + 2 * i]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  int slot = 0;
-  if (blockIdx.x < p.n_tiles) {
+  int slot = 0, it = 0;
+  if (NBUF == 2 && blockIdx.x < p.n_tiles) {
     decode(blockIdx.x, 0);
     __syncthreads();
-    issue_loads(0);
+    issue_loads(0, 0);
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, slot ^= 1) {
-    const int64_t tn = t + gridDim.x;
-    if (tn < p.n_tiles) decode(tn, slot ^ 1);
-    __syncthreads();  // next base visible; previous store phase done with slot ^ 1
-    if (tn < p.n_tiles) issue_loads(slot ^ 1);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+    if (NBUF == 2) {
+      const int64_t tn = t + gridDim.x;
+      if (tn < p.n_tiles) decode(tn, (it + 1) & 3);
+      __syncthreads();  // next base visible; previous store phase done with slot ^ 1
+      if (tn < p.n_tiles) {
+        issue_loads(slot ^ 1, (it + 1) & 3);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+    } else {
+      decode(t, it & 3);
+      __syncthreads();  // base visible; previous store phase done with the tile
+      issue_loads(0, it & 3);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();  // tile t resident
     float2* tile = tiles + slot * kTile;
-    float2* dst = out + s_base[slot][1];
-    float2 v[kPer];
+    float2* dst = out + s_base[it & 3][1] + my_out_lo;
+    float2 c[kCube];
     for (int g = 0; g < p.n_groups; ++g) {
-      const int b0 = p.group_bits[g][0], b1 = p.group_bits[g][1];
-      const int b2 = p.group_bits[g][2], b3 = p.group_bits[g][3];
-      for (int q = tid; q < kTile / 16; q += kThreadsAbs) {
-        // insert zero bits at b0 < b1 < b2 < b3 into the 8-bit cube index q
-        int base = q;
-        base = ((base >> b0) << (b0 + 1)) | (base & ((1 << b0) - 1));
-        base = ((base >> b1) << (b1 + 1)) | (base & ((1 << b1) - 1));
-        base = ((base >> b2) << (b2 + 1)) | (base & ((1 << b2) - 1));
-        base = ((base >> b3) << (b3 + 1)) | (base & ((1 << b3) - 1));
-        float2 c[16];
+      int sb[kCubeBits];
 #pragma unroll
-        for (int s = 0; s < 16; ++s)
-          c[s] = tile[swz(base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
-                          (((s >> 3) & 1) << b3))];
-        for (int k = p.group_gates[g][0]; k < p.group_gates[g][1]; ++k) apply_gate(c, p.gate_local[k], p.u[k]);
+      for (int j = 0; j < kCubeBits; ++j) sb[j] = p.group_cube[g][j];
+      int b0 = 0;
 #pragma unroll
-        for (int s = 0; s < 16; ++s)
-          tile[swz(base | ((s & 1) << b0) | (((s >> 1) & 1) << b1) | (((s >> 2) & 1) << b2) |
-                   (((s >> 3) & 1) << b3))] = c[s];
+      for (int j = 0; j < kThreadBits; ++j)
+        if ((tid >> j) & 1) b0 ^= p.group_lane[g][j];
+#pragma unroll
+      for (int s = 0; s < kCube; ++s) {
+        int a = b0;
+#pragma unroll
+        for (int j = 0; j < kCubeBits; ++j)
+          if ((s >> j) & 1) a ^= sb[j];
+        c[s] = tile[a];
+      }
+      for (int k = p.group_gates[g][0]; k < p.group_gates[g][1]; ++k) apply_gate(c, p.gate_local[k], p.u[k]);
+#pragma unroll
+      for (int s = 0; s < kCube; ++s) {
+        int a = b0;
+#pragma unroll
+        for (int j = 0; j < kCubeBits; ++j)
+          if ((s >> j) & 1) a ^= sb[j];
+        tile[a] = c[s];
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int f = tid + i * kThreadsAbs;
-      v[i] = tile[swz(t_src_lo[f & 63] | t_src_hi[f >> 6])];
-    }
+    for (int i = 0; i < kPer; ++i) c[i] = tile[my_src_lo ^ t_src_hi[hi0 + 2 * i]];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int f = tid + i * kThreadsAbs;
-      dst[t_out_lo[f & 63] + t_out_hi[f >> 6]] = v[i];
-    }
+    for (int i = 0; i < kPer; ++i) dst[t_out_hi[hi0 + 2 * i]] = c[i];
+    if (NBUF == 2) slot ^= 1;
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (NBUF == 2) asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 struct GateRef {
@@ -325,38 +371,73 @@ int launch_pass(int r, const Section& sec, const std::vector<GateRef>& gates, co
     p.in_hi[i] = hi;
     p.out_lo[i] = olo;
     p.out_hi[i] = ohi;
-    p.src_lo[i] = slo;
-    p.src_hi[i] = shi;
+    p.src_lo[i] = swz(slo);  // swz is XOR-linear: swz(lo | hi) = swz(lo) ^ swz(hi)
+    p.src_hi[i] = swz(shi);
   }
-  // group consecutive gates whose legs span <= 4 tile bits
+  // group consecutive gates whose legs span <= kCubeBits tile bits
   const int n_gates = static_cast<int>(sec.gates.size());
   std::vector<int> cur_bits;
   p.n_groups = 0;
   auto close_group = [&](int end) {
     if (cur_bits.empty()) return;
+    // Bank conflicts: a 64-bit smem access is served per 16 lanes, and the
+    // bank slot of tile bit t is (t mod 4) under swz; lanes 0..15 (thread bits
+    // 0..3) must therefore sit on four tile bits of distinct t mod 4.  Pick
+    // the cube's filler bits so that the remaining bits keep every class.
     std::vector<int> bits = cur_bits;
-    for (int b = 0; static_cast<int>(bits.size()) < 4; ++b)
-      if (std::find(bits.begin(), bits.end(), b) == bits.end()) bits.push_back(b);
+    auto in = [](const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); };
+    while (static_cast<int>(bits.size()) < kCubeBits) {
+      int best = -1, best_left = -1;
+      for (int t = 0; t < kTileBits; ++t) {
+        if (in(bits, t)) continue;
+        int left = 0;  // free bits of t's class after taking t
+        for (int u = 0; u < kTileBits; ++u)
+          if (u != t && !in(bits, u) && (u & 3) == (t & 3)) ++left;
+        if (left > best_left) best = t, best_left = left;
+      }
+      bits.push_back(best);
+    }
     std::sort(bits.begin(), bits.end());
+    std::vector<int> lanes;
+    for (int cls = 0; cls < 4; ++cls)
+      for (int t = 0; t < kTileBits; ++t)
+        if (!in(bits, t) && !in(lanes, t) && (t & 3) == cls) {
+          lanes.push_back(t);
+          break;
+        }
+    for (int t = 0; t < kTileBits; ++t)
+      if (!in(bits, t) && !in(lanes, t)) lanes.push_back(t);
     const int g = p.n_groups;
-    for (int i = 0; i < 4; ++i) p.group_bits[g][i] = bits[i];
+    for (int i = 0; i < kCubeBits; ++i) p.group_cube[g][i] = swz(1 << bits[i]);
+    for (int i = 0; i < kThreadBits; ++i) p.group_lane[g][i] = swz(1 << lanes[i]);
     p.group_gates[g][1] = end;
     for (int k = p.group_gates[g][0]; k < end; ++k) {
       const GateRef& gr = gates[sec.gates[k]];
-      const int la = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pa]) - bits.begin());
-      const int lb = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pb]) - bits.begin());
-      p.gate_local[k] = 4 * la + lb;
+      int la = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pa]) - bits.begin());
+      int lb = static_cast<int>(std::find(bits.begin(), bits.end(), bit_of[gr.pb]) - bits.begin());
+      float2 u[16];
+      std::memcpy(u, gr.u, sizeof(u));  // host gate data baked into the launch
+      // orient the gate so in_a is the lower local bit: swapping the roles of
+      // (a, b) transposes both the output and the input index pair of U
+      const bool swap = la > lb;
+      if (swap) std::swap(la, lb);
+      auto q = [&](int x) { return swap ? (((x & 1) << 1) | (x >> 1)) : x; };
+      for (int o = 0; o < 4; ++o)
+        for (int i = 0; i < 4; ++i) {
+          const float2 e = u[q(o) * 4 + q(i)];
+          p.u[k][o * 4 + i] = make_float4(e.x, e.y, -e.y, e.x);
+        }
+      p.gate_local[k] = 8 * la + lb;
     }
     ++p.n_groups;
     cur_bits.clear();
   };
   for (int k = 0; k < n_gates; ++k) {
     const GateRef& gr = gates[sec.gates[k]];
-    std::memcpy(p.u[k], gr.u, 16 * sizeof(float2));  // host gate data baked into the launch
     std::vector<int> trial = cur_bits;
     for (int b : {bit_of[gr.pa], bit_of[gr.pb]})
       if (std::find(trial.begin(), trial.end(), b) == trial.end()) trial.push_back(b);
-    if (trial.size() > 4) {
+    if (static_cast<int>(trial.size()) > kCubeBits) {
       close_group(k);
       trial = {bit_of[gr.pa], bit_of[gr.pb]};
     }
@@ -375,13 +456,24 @@ int launch_pass(int r, const Section& sec, const std::vector<GateRef>& gates, co
     p.outer_out[i] = out_stride[outer[i]];
   }
   p.n_tiles = static_cast<int64_t>(1) << p.n_outer;
-  const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()) * 4);
   ProfScope prof(PROF_ABSORB, 32.0 * n_gates * (static_cast<double>(1) * (int64_t(1) << r)),
                  16.0 * static_cast<double>(int64_t(1) << r), stream);
-  const size_t smem = 2 * kTile * sizeof(float2);
-  TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-  absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreadsAbs, smem, stream>>>(in, out, p);
+  static const int nbuf = [] {
+    const char* e = std::getenv("TNC_ABSORB_NBUF");
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
+  const size_t smem = static_cast<size_t>(nbuf) * kTile * sizeof(float2);
+  const int per_sm = nbuf == 2 ? 3 : 4;  // smem (NBUF 2) or register (NBUF 1) limited residency
+  const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()) * per_sm);
+  if (nbuf == 2) {
+    TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    absorb_pass_kernel<2><<<static_cast<unsigned>(blocks), kThreadsAbs, smem, stream>>>(in, out, p);
+  } else {
+    TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    absorb_pass_kernel<1><<<static_cast<unsigned>(blocks), kThreadsAbs, smem, stream>>>(in, out, p);
+  }
   TNC_CHECK_LAUNCH();
   return TNC_OK;
 }

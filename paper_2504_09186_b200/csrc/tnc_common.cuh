@@ -87,7 +87,8 @@ struct Axis {
 
 // ---- optional per-kernel device timing (tnc_profile_*) ----
 enum ProfKind { PROF_TC_GEMM = 0, PROF_SIMT_GEMM = 1, PROF_PERMUTE = 2, PROF_SPLIT_PREP = 3,
-                PROF_REDUCE = 4, PROF_ABSORB = 5, PROF_AXPY = 6, PROF_KINDS = 7 };
+                PROF_REDUCE = 4, PROF_ABSORB = 5, PROF_AXPY = 6, PROF_STREAM = 7,
+                PROF_KINDS = 8 };
 // RAII: when profiling is enabled, records CUDA events around the launches
 // issued in its scope on `stream` and books `flops` / `bytes` of algorithmic
 // work to `kind`.
@@ -148,6 +149,17 @@ int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const 
 // fixed-order pairwise tree reduction of P partial [M,N] fp32-complex buffers
 int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out_or_null,
                        int64_t M, int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream);
+
+// K5 narrow-step streaming contraction (tnc_stream.cu).  Leg kinds: 0 =
+// X-free, 1 = common, 2 = Y-free; extents are all 2.
+struct StreamLeg {
+  int kind;
+  int64_t x_stride, y_stride, out_stride;
+};
+struct StreamPlan;
+int stream_prepare(int n_legs, const StreamLeg* legs, StreamPlan** out);
+void stream_destroy(StreamPlan* sp);
+int stream_launch(const StreamPlan* sp, const void* x, const void* y, void* c, cudaStream_t stream);
 
 // K4 step fusion (tnc_absorb.cu)
 int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t* bytes);

@@ -106,32 +106,42 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;
 }
 
-template <bool F16>
-__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  if constexpr (F16) {
+// Whole-warp variants: every lane runs the (warp-uniform) issue loop and
+// elect.sync picks the issuing lane inside the asm, so the compiler keeps the
+// operands in uniform registers instead of wrapping each MMA in a
+// single-lane waterfall loop (ncu: ~15 dependent instructions per MMA).
+template <int CG, bool F16>
+__device__ __forceinline__ void mma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  if constexpr (CG == 1 && F16) {
     asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
+        "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else if constexpr (CG == 1) {
+    asm volatile(
+        "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else if constexpr (F16) {
+    asm volatile(
+        "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   } else {
     asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
+        "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   }
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -265,46 +275,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      uint32_t it = 0, ch = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int split, mb, nb;
-        decode_unit(p, u, split, mb, nb);
-        const int kb_lo = split * p.kb_per_split;
-        const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
-        int in_chunk = 0;
-        uint32_t dcol = 0;
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
-          if (in_chunk == 0) {
-            const uint32_t b = ch & 1;
-            mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            dcol = tmem_base + b * BN;
-          }
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&full[s], ph);
+    // whole warp, warp-uniform control flow; one elected lane issues
+    const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint64_t dhi = umma_desc<SWZ>(0);  // descriptor without the address field
+    const uint32_t smem0 = smem_u32(smem);
+    uint32_t it = 0, ch = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int split, mb, nb;
+      decode_unit(p, u, split, mb, nb);
+      const int kb_lo = split * p.kb_per_split;
+      const int kb_hi = min(p.num_kb, kb_lo + p.kb_per_split);
+      int in_chunk = 0;
+      uint32_t dcol = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+        if (in_chunk == 0) {
+          const uint32_t b = ch & 1;
+          mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(smem + s * Cfg::kStageBytes);
-          const uint32_t a_big = st, a_small = st + Cfg::kABytes;
-          const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
+          dcol = tbase + b * BN;
+        }
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = smem0 + s * Cfg::kStageBytes;
+        // address field = bits [0,14) of (addr >> 4); 32 bytes of K = +2
+        const uint64_t a_big = dhi | ((st >> 4) & 0x3FFF);
+        const uint64_t a_small = dhi | (((st + Cfg::kABytes) >> 4) & 0x3FFF);
+        const uint64_t b_big = dhi | (((st + 2 * Cfg::kABytes) >> 4) & 0x3FFF);
+        const uint64_t b_small = dhi | (((st + 2 * Cfg::kABytes + Cfg::kBBytes) >> 4) & 0x3FFF);
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kMmaPerKb; ++kk) {
-            const uint32_t off = kk * 32;  // 8 tf32 / 16 f16 = 32 bytes along the swizzled row
-            const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
-            mma_issue<F16>(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc,
-                     acc0);
-            mma_issue<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off), Cfg::kIdesc,
-                     1u);
-            mma_issue<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off), Cfg::kIdesc, 1u);
-          }
-          mma_commit(&empty[s]);
-          ++in_chunk;
-          if (in_chunk == p.kb_per_chunk || kb + 1 == kb_hi) {
-            mma_commit(&tfull[ch & 1]);
-            ++ch;
-            in_chunk = 0;
-          }
+        for (int kk = 0; kk < Cfg::kMmaPerKb; ++kk) {
+          const uint64_t o = 2 * kk;
+          const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
+          mma_elect<1, F16>(dcol, a_small + o, b_big + o, Cfg::kIdesc, acc0);
+          mma_elect<1, F16>(dcol, a_big + o, b_small + o, Cfg::kIdesc, 1u);
+          mma_elect<1, F16>(dcol, a_big + o, b_big + o, Cfg::kIdesc, 1u);
+        }
+        mma_commit_elect(&empty[s]);
+        ++in_chunk;
+        if (in_chunk == p.kb_per_chunk || kb + 1 == kb_hi) {
+          mma_commit_elect(&tfull[ch & 1]);
+          ++ch;
+          in_chunk = 0;
         }
       }
     }
@@ -460,31 +473,10 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, uint64_t
       : "memory");
 }
 
-template <bool F16>
-__device__ __forceinline__ void mma_issue_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                              uint32_t idesc, uint32_t accumulate) {
-  if constexpr (F16) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-  } else {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-  }
-}
-
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_2sm_elect(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
           smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
       : "memory");
@@ -578,7 +570,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
+      // whole warp, warp-uniform control flow; one elected lane issues
+      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint64_t dhi = umma_desc<SWZ>(0);
+      const uint32_t smem0 = smem_u32(smem);
       uint32_t it = 0, ch = 0;
       for (int u = pair; u < units; u += pairs) {
         int split, mb, nb;
@@ -592,30 +588,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b = ch & 1;
             mbar_wait_cluster(&tempty[b], ((ch >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            dcol = tmem_base + b * BN;
+            dcol = tbase + b * BN;
           }
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(smem + s * Cfg::kStageBytes);
-          const uint32_t a_big = st, a_small = st + Cfg::kABytes;
-          const uint32_t b_big = st + 2 * Cfg::kABytes, b_small = b_big + Cfg::kBBytes;
+          const uint32_t st = smem0 + s * Cfg::kStageBytes;
+          const uint64_t a_big = dhi | ((st >> 4) & 0x3FFF);
+          const uint64_t a_small = dhi | (((st + Cfg::kABytes) >> 4) & 0x3FFF);
+          const uint64_t b_big = dhi | (((st + 2 * Cfg::kABytes) >> 4) & 0x3FFF);
+          const uint64_t b_small = dhi | (((st + 2 * Cfg::kABytes + Cfg::kBBytes) >> 4) & 0x3FFF);
 #pragma unroll
           for (int kk = 0; kk < Cfg::kMmaPerKb; ++kk) {
-            const uint32_t off = kk * 32;
+            const uint64_t o = 2 * kk;
             const uint32_t acc0 = (in_chunk > 0 || kk > 0) ? 1u : 0u;
-            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_small + off), umma_desc<SWZ>(b_big + off),
-                               Cfg::kIdesc, acc0);
-            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_small + off),
-                               Cfg::kIdesc, 1u);
-            mma_issue_2sm<F16>(dcol, umma_desc<SWZ>(a_big + off), umma_desc<SWZ>(b_big + off),
-                               Cfg::kIdesc, 1u);
+            mma_elect<2, F16>(dcol, a_small + o, b_big + o, Cfg::kIdesc, acc0);
+            mma_elect<2, F16>(dcol, a_big + o, b_small + o, Cfg::kIdesc, 1u);
+            mma_elect<2, F16>(dcol, a_big + o, b_big + o, Cfg::kIdesc, 1u);
           }
-          mma_commit_2sm(&empty[s]);
+          mma_commit_2sm_elect(&empty[s]);
           ++in_chunk;
           if (in_chunk == p.kb_per_chunk || kb + 1 == kb_hi) {
-            mma_commit_2sm(&tfull[ch & 1]);
+            mma_commit_2sm_elect(&tfull[ch & 1]);
             ++ch;
             in_chunk = 0;
           }

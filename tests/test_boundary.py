@@ -74,6 +74,22 @@ def test_plan_shapes_and_output_order_host_only():
     # tiny output, huge K -> the CUDA-core split-K reduction is auto-selected
     code, info, _ = _plan([("m", 2)] + [(f"k{i}", 2) for i in range(14)], [(f"k{i}", 2) for i in range(14)] + [("n", 4)])
     assert code == 0 and info.variant == 3
+    # narrow step (C1a-like): the K5 streaming kernel, no workspace at all
+    code, info, _ = _plan([(f"a{i}", 2) for i in range(16)] + [(f"k{i}", 2) for i in range(6)],
+                          [(f"k{i}", 2) for i in range(6)] + [(f"b{i}", 2) for i in range(4)],
+                          out=[f"b{i}" for i in range(4)] + [f"a{i}" for i in range(16)])
+    assert code == 0 and info.variant == 5 and info.workspace_bytes == 0
+
+
+def test_stream_variant_rejects_oversized_y():
+    """Forcing the streaming variant when Y cannot sit on chip (rows_y * K =
+    2^14 > 4096) is an explicit UNSUPPORTED status, never a silent fallback."""
+    a = [(f"a{i}", 2) for i in range(12)] + [(f"k{i}", 2) for i in range(8)]
+    b = [(f"k{i}", 2) for i in range(8)] + [(f"b{i}", 2) for i in range(6)]
+    code, _, _ = _plan(a, b, variant=5)
+    assert code == 8
+    code, _, _ = _plan([("a", 3), ("k", 2)], [("k", 2), ("b", 2)], variant=5)  # extent-3 leg
+    assert code == 8
 
 
 def test_plan_errors_map_to_reference_exceptions():
