@@ -351,7 +351,10 @@ def bench_c3(args) -> None:
                        "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_eff, "unit": "TFLOP/s",
-                         "frac": (achieved / p_eff) if achieved else None, "traffic": None,
+                         "frac": (achieved / p_eff) if achieved else None,
+                         "traffic": _profiled_traffic(args.workload),
+                         "traffic_source": "profiles/r01_tc_traffic.json (ncu dram__bytes_read+write per "
+                                           "tc_cgemm launch, C3 slice)" if args.workload == "c3" else None,
                          "kernel": kernel_name, "peak_source": peak_source,
                          "launches": tc["launches"], "share_of_step": tc["ms"] / 1e3 / elapsed},
             "kernels": prof, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
@@ -461,6 +464,16 @@ def bench_c1(args) -> None:
                               m.bit_length() - 1, k.bit_length() - 1, n.bit_length() - 1], "kernels": prof}),
               flush=True)
         del a, b, out
+
+
+def _profiled_traffic(workload: str):
+    """DRAM bytes per tensor-core GEMM launch from the committed ncu capture of
+    this same command (profiles/r01_tc_traffic.json); None when not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_tc_traffic.json")
+    if workload != "c3" or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get("dram_bytes_per_launch")
 
 
 def _read_prof(lib) -> dict:
