@@ -70,7 +70,7 @@ __device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gmem_sr
 }
 
 // 128 registers (2 CTAs / SM); a 3-CTA register cap spills and measured 2x slower
-template <int KS>
+template <int KS, int RP>
 __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __restrict__ X,
                                                             const float2* __restrict__ Y,
                                                             float2* __restrict__ C,
@@ -83,16 +83,8 @@ __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __r
   const int buf_elems = R * p.kpad;
   // tile bases ring-indexed by iteration (see absorb_pass_kernel)
   __shared__ int64_t s_base[4][2];
-  __shared__ int64_t t_in_hi[64], t_out_hi[64];
-  __shared__ int t_pos_hi[64], t_src_hi[64];
   __shared__ int64_t s_ox[TNC_MAX_RANK], s_oo[TNC_MAX_RANK];
   const int tid = threadIdx.x;
-  if (tid < 64) {
-    t_in_hi[tid] = p.in_hi[tid];
-    t_out_hi[tid] = p.out_hi[tid];
-    t_pos_hi[tid] = p.pos_hi[tid];
-    t_src_hi[tid] = p.src_hi[tid];
-  }
   if (tid < p.n_outer) {
     s_ox[tid] = p.outer_x[tid];
     s_oo[tid] = p.outer_out[tid];
@@ -112,12 +104,15 @@ __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __r
     yre[q] = v.x;
     yim[q] = pack2(-v.y, v.y);
   }
-  const int64_t my_in_lo = p.in_lo[tid & 63];
-  const int my_pos_lo = p.pos_lo[tid & 63];
-  const int64_t my_out_lo = p.out_lo[tid & 63];
-  const int my_src_lo = p.src_lo[tid & 63];
-  const int hi0 = tid >> 6;  // kThreadsSt = 4 * 64: high table index = hi0 + 4 i
-  const int rows_per = R / p.groups;
+  // element e = tid + 256 i: low 6 bits tid & 63, high 6 bits (tid >> 6) + 4 i.
+  // The maps are sums of per-bit strides, so the high-table entry splits into
+  // a per-thread part (bits 0-1) and a uniform part (bits 2-5) that the
+  // unrolled loops read as constant-bank operands.
+  const int hi0 = tid >> 6;
+  const int64_t my_in = p.in_lo[tid & 63] + p.in_hi[hi0];
+  const int my_pos = p.pos_lo[tid & 63] + p.pos_hi[hi0];
+  const int64_t my_out = p.out_lo[tid & 63] + p.out_hi[hi0];
+  const int my_src = p.src_lo[tid & 63] + p.src_hi[hi0];
   const int tile_elems = R * K, out_elems = R * N;
   const uint32_t sm_s = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
   auto decode = [&](int64_t t, int slot) {
@@ -140,10 +135,13 @@ __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __r
     }
   };
   auto issue_loads = [&](int buf, int slot) {
-    const float2* src = X + s_base[slot][0] + my_in_lo;
-    const uint32_t dst = sm_s + 8u * static_cast<uint32_t>(buf * buf_elems + my_pos_lo);
-    for (int i = 0; tid + i * kThreadsSt < tile_elems; ++i)
-      cp_async8(dst + 8u * static_cast<uint32_t>(t_pos_hi[hi0 + 4 * i]), src + t_in_hi[hi0 + 4 * i]);
+    const float2* src = X + s_base[slot][0] + my_in;
+    const uint32_t dst = sm_s + 8u * static_cast<uint32_t>(buf * buf_elems + my_pos);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (tid + i * kThreadsSt >= tile_elems) break;
+      cp_async8(dst + 8u * static_cast<uint32_t>(p.pos_hi[4 * i]), src + p.in_hi[4 * i]);
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   __syncthreads();
@@ -168,10 +166,11 @@ __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __r
     float2* xs = sm + buf * buf_elems;
     float2* part = p.part_alias ? xs : sm + 2 * buf_elems;
     // math: rows grp, grp + G, ... ; k in this thread's slice
-    float2 res[kMaxRowsPer];
+    // RP rows per thread, compile-time: the whole block of row loads and
+    // FFMA2 chains is straight-line code the scheduler can overlap
+    float2 res[RP];
 #pragma unroll
-    for (int rr = 0; rr < kMaxRowsPer; ++rr) {
-      if (rr >= rows_per) break;
+    for (int rr = 0; rr < RP; ++rr) {
       const int r = grp + rr * p.groups;
       const float4* xr = reinterpret_cast<const float4*>(xs + r * p.kpad + slc * KS);
       u64 acc0 = 0, acc1 = 0;
@@ -191,21 +190,22 @@ __global__ void __launch_bounds__(kThreadsSt, 2) stream_kernel(const float2* __r
     }
     if (p.part_alias) __syncthreads();  // every thread is done reading the X tile
 #pragma unroll
-    for (int rr = 0; rr < kMaxRowsPer; ++rr) {
-      if (rr >= rows_per) break;
+    for (int rr = 0; rr < RP; ++rr) {
       part[(slc * R + grp + rr * p.groups) * p.npitch + j] = res[rr];
     }
     __syncthreads();
     // store in output order; sum the k-slice partials in fixed order
-    for (int i = 0; tid + i * kThreadsSt < out_elems; ++i) {
-      const int sidx = my_src_lo + t_src_hi[hi0 + 4 * i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (tid + i * kThreadsSt >= out_elems) break;
+      const int sidx = my_src + p.src_hi[4 * i];
       float2 v = part[sidx];
       for (int s = 1; s < p.slices; ++s) {
         const float2 w = part[s * R * p.npitch + sidx];
         v.x += w.x;
         v.y += w.y;
       }
-      C[obase + my_out_lo + t_out_hi[hi0 + 4 * i]] = v;
+      C[obase + my_out + p.out_hi[4 * i]] = v;
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -358,13 +358,23 @@ int stream_launch(const StreamPlan* sp, const void* x, const void* y, void* c, c
     TNC_CHECK_LAUNCH();
     return TNC_OK;
   };
-  switch (sp->ks) {
-    case 1: return go(stream_kernel<1>);
-    case 2: return go(stream_kernel<2>);
-    case 4: return go(stream_kernel<4>);
-    case 8: return go(stream_kernel<8>);
-    default: return go(stream_kernel<16>);
+  const int rp = (1 << p.t) / p.groups;
+#define TNC_STREAM_RP(KS_)                           \
+  switch (rp) {                                      \
+    case 1: return go(stream_kernel<KS_, 1>);        \
+    case 2: return go(stream_kernel<KS_, 2>);        \
+    case 4: return go(stream_kernel<KS_, 4>);        \
+    case 8: return go(stream_kernel<KS_, 8>);        \
+    default: return go(stream_kernel<KS_, 16>);      \
   }
+  switch (sp->ks) {
+    case 1: TNC_STREAM_RP(1)
+    case 2: TNC_STREAM_RP(2)
+    case 4: TNC_STREAM_RP(4)
+    case 8: TNC_STREAM_RP(8)
+    default: TNC_STREAM_RP(16)
+  }
+#undef TNC_STREAM_RP
 }
 
 }  // namespace tnc
