@@ -159,8 +159,6 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
   __shared__ int64_t s_base[4][2];
   // per-element table lookups must not hit the (serialising) param/constant
   // bank with divergent addresses: stage the tables in shared memory
-  __shared__ int64_t t_in_hi[64], t_out_hi[64];
-  __shared__ int t_src_hi[64];
   __shared__ int64_t s_oin[TNC_MAX_RANK], s_oout[TNC_MAX_RANK];
   __shared__ int s_oshift[TNC_MAX_RANK];
   const int tid = threadIdx.x;
@@ -170,18 +168,15 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
     s_oout[tid] = p.outer_out[tid];
     s_oshift[tid] = p.outer_shift[tid];
   }
-  if (tid < 64) {
-    t_in_hi[tid] = p.in_hi[tid];
-    t_out_hi[tid] = p.out_hi[tid];
-    t_src_hi[tid] = p.src_hi[tid];
-  }
   // element e = tid + kThreadsAbs * i: its low 6 bits are the thread's own
   // (kThreadsAbs is a multiple of 64), its high 6 bits are (tid >> 6) + 2 i
-  const int64_t my_in_lo = p.in_lo[tid & 63];
+  // high-table entry (tid >> 6) + 2 i splits into a per-thread part (bit 0)
+  // and a uniform part (bits 1-5) read as constant-bank operands: the maps are
+  // sums (offsets) / XORs (swizzled slots) of per-bit terms
+  const int64_t my_in_lo = p.in_lo[tid & 63] + p.in_hi[tid >> 6];
   const int my_swz = swz(tid);
-  const int64_t my_out_lo = p.out_lo[tid & 63];
-  const int my_src_lo = p.src_lo[tid & 63];
-  const int hi0 = tid >> 6;
+  const int64_t my_out_lo = p.out_lo[tid & 63] + p.out_hi[tid >> 6];
+  const int my_src_lo = p.src_lo[tid & 63] ^ p.src_hi[tid >> 6];
   const uint32_t tiles_s = static_cast<uint32_t>(__cvta_generic_to_shared(tiles));
   __syncthreads();
   constexpr int kPer = kTile / kThreadsAbs;
@@ -210,7 +205,7 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
     const uint32_t dst = tiles_s + slot * kTile * 8;
 #pragma unroll
     for (int i = 0; i < kPer; ++i)
-      cp_async8(dst + ((my_swz ^ swz(kThreadsAbs * i)) << 3), src + t_in_hi[hi0 + 2 * i]);
+      cp_async8(dst + ((my_swz ^ swz(kThreadsAbs * i)) << 3), src + p.in_hi[2 * i]);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int slot = 0, it = 0;
@@ -268,9 +263,9 @@ __global__ void __launch_bounds__(kThreadsAbs) absorb_pass_kernel(const float2* 
       __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) c[i] = tile[my_src_lo ^ t_src_hi[hi0 + 2 * i]];
+    for (int i = 0; i < kPer; ++i) c[i] = tile[my_src_lo ^ p.src_hi[2 * i]];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) dst[t_out_hi[hi0 + 2 * i]] = c[i];
+    for (int i = 0; i < kPer; ++i) dst[p.out_hi[2 * i]] = c[i];
     if (NBUF == 2) slot ^= 1;
   }
   if (NBUF == 2) asm volatile("cp.async.wait_group 0;" ::: "memory");
