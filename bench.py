@@ -239,7 +239,30 @@ def bench_c3(args) -> None:
     lib = _lib.load(require_device=True)
     wl, net, t, s, spec, per_slice, slice_ids = plan_workload(args.workload)
     order = wl.output_order()
-    ex = SliceExecutor(net, s, spec, "single", order)
+    reuse_info = None
+    if args.reuse > 0:
+        # spindle reuse (the paper's data reuse, reference reuse.py): a unit of
+        # work is one reuse program over prod(nested dims) slices
+        from paper_2504_09186_b200 import choose_reuse_subset, plan_spindle
+        from paper_2504_09186_b200.execute import ReuseRunner
+
+        part_ = choose_reuse_subset(t, spec, None, args.reuse)
+        rs, rep = plan_spindle(part_.schedule, part_.spec, None, nested_labels=part_.nested_labels)
+        ex = ReuseRunner(net, rs, "single", order)
+        unit_slices = ex.slices_per_program
+        n_units = ex.n_programs
+        if n_units * unit_slices <= 4096:
+            slice_ids = list(range(n_units))
+        else:
+            slice_ids = sorted(int(x) for x in np.random.default_rng(0).choice(
+                n_units, max(1, 1024 // unit_slices), replace=False))
+        reuse_info = {"nested_labels": [e.index.label for e in rs.nested], "slices_per_program": unit_slices,
+                      "programs_sampled": len(slice_ids),
+                      "multiplies_saved_factor": float(per_slice * spec.n_subtasks / rep.predicted_multiplies),
+                      "predicted_peak_gib": rep.predicted_peak_bytes / 2**30}
+    else:
+        ex = SliceExecutor(net, s, spec, "single", order)
+        unit_slices = 1
     ex.prepare()
     n_ids = len(slice_ids)
     spp = args.slices_per_step
@@ -259,6 +282,7 @@ def bench_c3(args) -> None:
         sampler.start()
     lib.tnc_profile_enable(1)
     launches0 = lib.tnc_launch_count()
+    mult0 = ex.stats.multiplies
     stream = torch.cuda.current_stream()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -271,6 +295,7 @@ def bench_c3(args) -> None:
     stop.record(stream)
     torch.cuda.synchronize()
     launches = lib.tnc_launch_count() - launches0
+    executed_mult = ex.stats.multiplies - mult0
     elapsed = start.elapsed_time(stop) / 1e3
     if world > 1:
         tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
@@ -280,7 +305,7 @@ def bench_c3(args) -> None:
     clocks = sampler.stop() if sampler else None
     prof = _read_prof(lib)
     lib.tnc_profile_enable(0)
-    slices_total = args.steps * spp * world
+    slices_total = args.steps * spp * world * unit_slices
     flops_total = 8 * per_slice * slices_total
     value = flops_total / elapsed / 1e12
 
@@ -299,14 +324,19 @@ def bench_c3(args) -> None:
         for i in range(args.e2e_steps):
             dev = [DenseTensor.__new__(DenseTensor)._init_raw(tt_.indices, hl.to("cuda", non_blocking=True))
                    for tt_, hl in zip(net.tensors, host_leaves)]
-            amps = run_open(TensorNetwork(dev), t, spec, order, "single", slice_ids=[slice_ids[i % n_ids]]).data.cpu()
+            if reuse_info is None:
+                amps = run_open(TensorNetwork(dev), t, spec, order, "single",
+                                slice_ids=[slice_ids[i % n_ids]]).data.cpu()
+            else:
+                rr = ReuseRunner(TensorNetwork(dev), rs, "single", order)
+                amps = rr.finish(rr.run([slice_ids[i % n_ids]])).data.cpu()
             d2h = amps.numel() * amps.element_size()
         e_e.record()
         torch.cuda.synchronize()
         e_t = e_s.elapsed_time(e_e) / 1e3
-        e2e = {"value": 8 * per_slice * args.e2e_steps / e_t / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": 8 * per_slice * unit_slices * args.e2e_steps / e_t / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "slices_per_s": args.e2e_steps / e_t}
+               "slices_per_s": unit_slices * args.e2e_steps / e_t}
 
     if rank == 0:
         peaks = measured_peaks()
@@ -346,7 +376,9 @@ def bench_c3(args) -> None:
             "config": {"workload": WORKLOAD_TEXT[args.workload],
                        "total_slices": spec.n_subtasks,
                        "extrapolated_hours_all_slices_this_job": spec.n_subtasks / (slices_total / elapsed) / 3600,
-                       "slices_per_step_per_gpu": spp, "slices_per_s": slices_total / elapsed,
+                       "slices_per_step_per_gpu": spp * unit_slices, "slices_per_s": slices_total / elapsed,
+                       "spindle_reuse": reuse_info,
+                       "executed_tflops": (8 * executed_mult / elapsed / 1e12) if reuse_info else None,
                        "flops_per_slice": 8 * per_slice, "l2": "inputs > L2 (intermediates up to 8 GiB)",
                        "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce"},
             "gpu_launches": int(launches),
@@ -500,6 +532,8 @@ def main() -> None:
     ap.add_argument("--cpu-cap", type=int, default=26)
     ap.add_argument("--ref-cap", type=int, default=25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reuse", type=int, default=0,
+                    help="spindle reuse with this many nested sliced labels (0: slice-invariant reuse only)")
     args = ap.parse_args()
     import paper_2504_09186_b200._lib as _l  # noqa: F401  (fail fast if the package is broken)
     if args.impl == "reference":

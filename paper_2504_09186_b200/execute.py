@@ -127,12 +127,22 @@ class Engine:
         return DenseTensor.__new__(DenseTensor)._init_raw(plan.out_indices, contract_into(plan, lhs.data, rhs.data))
 
     def run_range(self, s: LinearSchedule, lo: int, hi: int, assignment: dict[str, int], values: dict,
-                  stats: RunStats, aux_bytes: int = 0) -> None:
-        """Steps lo..hi (1-based, inclusive) -- reference ``execute.py:137-178``."""
+                  stats: RunStats, aux_bytes: int = 0, cache: dict | None = None) -> None:
+        """Steps lo..hi (1-based, inclusive) -- reference ``execute.py:137-178``.
+        ``cache`` (slice-invariant step results, see ``ReuseRunner``) short-cuts
+        steps whose result no sliced label reaches."""
         rate = self.rate
         live = sum(v.size for v in values.values())
         for pos in range(lo - 1, hi):
             step = s.steps[pos]
+            if cache is not None and step.result in cache:
+                for ref in (step.lhs, step.rhs):
+                    if ref >= s.n_leaves and ref in values:
+                        live -= values[ref].size
+                        del values[ref]
+                values[step.result] = cache[step.result]
+                live += values[step.result].size
+                continue
             lhs = self.fetch(s, step.lhs, assignment, values)
             rhs = self.fetch(s, step.rhs, assignment, values)
             out_size = _result_size(lhs.indices, rhs.indices)
@@ -221,10 +231,13 @@ def _add(a: DenseTensor, b: DenseTensor) -> DenseTensor:
 
 
 def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets: dict[str, set[int]],
-                 mem_budget: int | None):
+                 mem_budget: int | None, open_root: bool = False, cache: dict | None = None):
     """Device interpreter of a reuse action program (reference
     ``execute.py:233-313``).  Tensors are immutable, so CHECKPOINT / STORE
-    keep references; MERGE sums the dependent values with the axpy kernel."""
+    keep references; MERGE sums the dependent values with the axpy kernel.
+
+    ``open_root`` (extension: the reference reduces scalar roots only) sums
+    tensor-valued roots of an open-output network on the device instead."""
     s = rs.schedule
     stats = RunStats()
     values: dict = {}
@@ -236,7 +249,14 @@ def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets
 
     def add_root(v):
         nonlocal acc
-        acc = v if acc is None else acc + v
+        if not open_root:
+            v = v.value()
+            acc = v if acc is None else acc + v
+        elif acc is None:
+            acc = DenseTensor.__new__(DenseTensor)._init_raw(v.indices, v.data.contiguous().clone())
+        else:
+            _lib.check(_lib.load().tnc_axpy(acc.dtype_code, acc.size, v.data.contiguous().data_ptr(),
+                                            acc.data.data_ptr(), _lib.stream_ptr()))
 
     def aux_bytes() -> int:
         seen = {}
@@ -249,7 +269,7 @@ def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets
         if act.kind == RUN:
             asn = dict(outer)
             asn.update(dict(act.assignment))
-            eng.run_range(s, act.lo, act.hi, asn, values, stats, aux_bytes())
+            eng.run_range(s, act.lo, act.hi, asn, values, stats, aux_bytes(), cache)
             parked = False
         elif act.kind == CHECKPOINT:
             snap = dict(values)
@@ -260,7 +280,7 @@ def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets
             cps[act.buf] = snap
         elif act.kind == RESTORE:
             if root in values and not parked:
-                add_root(values[root].value())
+                add_root(values[root])
             values = dict(cps[act.buf])
             parked = False
         elif act.kind == FREE:
@@ -287,7 +307,7 @@ def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets
         else:
             raise PlanningError(f"unknown action {act.kind}")
     if root in values:
-        add_root(values[root].value())
+        add_root(values[root])
     if acc is None:
         raise PlanningError("reuse program produced no final value")
     stats.subtasks_done = rs.nested_count
@@ -319,6 +339,100 @@ def run_reuse(net: TensorNetwork, t: ContractionTree, rs: ReuseSchedule, workers
     value = hierarchical_reduce(results, ReductionTopology(group_size))
     stats.wall_time = time.perf_counter() - t0
     return RunResult(value, stats, dict(zip(keys, results)), labels, dims)
+
+
+def run_reuse_open(net: TensorNetwork, t: ContractionTree, rs: ReuseSchedule,
+                   output_order: Sequence[str] | None = None, precision: str = "single",
+                   mem_budget: int | None = None) -> DenseTensor:
+    """Open-output spindle reuse: the reuse program of ``rs`` run once per
+    outer assignment, tensor roots summed on the device (outer programs in
+    enumeration order), permuted to ``output_order``.  Extension of
+    ``run_reuse`` (reference ``execute.py:316-372`` reduces scalar roots)."""
+    eng = Engine(net, precision)
+    labels = tuple(e.index.label for e in rs.outer)
+    dims = tuple(e.index.dim for e in rs.outer)
+    deps = {e.index.label: dependent_results(rs.schedule, e.index.label) for e in rs.nested}
+    total = None
+    for key in _slice_keys(dims):
+        part, _ = _run_program(eng, rs, dict(zip(labels, key)), deps, mem_budget, open_root=True)
+        if total is None:
+            total = part
+        else:
+            _lib.check(_lib.load().tnc_axpy(total.dtype_code, total.size, part.data.contiguous().data_ptr(),
+                                            total.data.data_ptr(), _lib.stream_ptr()))
+    if output_order is None:
+        return total
+    by = {ix.label: ix for ix in total.indices}
+    return permute(total, [by[l] for l in output_order])
+
+
+class ReuseRunner:
+    """Spindle-reuse scheduler for open outputs on one device: the reuse
+    program of ``rs`` (reference ``reuse.py:298-514`` / ``execute.py:233-313``)
+    run per outer assignment, on top of the slice-invariant cache of
+    ``SliceExecutor`` (steps no sliced label reaches run once in
+    :meth:`prepare`).  A program covers prod(nested dims) slices and runs the
+    steps after each MERGE once for all of them."""
+
+    def __init__(self, net: TensorNetwork, rs: ReuseSchedule, precision: str = "single",
+                 output_order: Sequence[str] | None = None, mem_budget: int | None = None):
+        self.rs = rs
+        self.s = rs.schedule
+        self.eng = Engine(net, precision)
+        self.output_order = list(output_order) if output_order is not None else None
+        self.mem_budget = mem_budget
+        labels = [e.index.label for e in rs.outer] + [e.index.label for e in rs.nested]
+        dep: set[int] = set()
+        for label in labels:
+            dep |= dependent_results(self.s, label)
+        self.invariant_positions = [p for p, st in enumerate(self.s.steps) if st.result not in dep]
+        self.deps = {e.index.label: dependent_results(self.s, e.index.label) for e in rs.nested}
+        self.outer_labels = tuple(e.index.label for e in rs.outer)
+        self.outer_dims = tuple(e.index.dim for e in rs.outer)
+        self.slices_per_program = product(e.index.dim for e in rs.nested)
+        self.n_programs = product(self.outer_dims)
+        self.cache: dict[int, DenseTensor] | None = None
+        self.stats = RunStats()
+
+    def prepare(self) -> None:
+        values: dict = {}
+        for p in self.invariant_positions:
+            self.eng.run_range(self.s, p + 1, p + 1, {}, values, self.stats)
+        self.cache = values
+
+    def outer_assignment(self, program_id: int) -> dict[str, int]:
+        """Mixed radix over the outer labels, first label most significant."""
+        out, rem = {}, program_id
+        for label, d in zip(reversed(self.outer_labels), reversed(self.outer_dims)):
+            out[label] = rem % d
+            rem //= d
+        return out
+
+    def run_program(self, program_id: int) -> DenseTensor:
+        if self.cache is None:
+            self.prepare()
+        root, st = _run_program(self.eng, self.rs, self.outer_assignment(program_id), self.deps,
+                                self.mem_budget, open_root=True, cache=self.cache)
+        self.stats.multiplies += st.multiplies
+        self.stats.subtasks_done += self.slices_per_program
+        return root
+
+    def run(self, program_ids: Iterable[int], acc: DenseTensor | None = None) -> DenseTensor:
+        total = acc
+        for pid in program_ids:
+            part = self.run_program(pid)
+            if total is None:
+                total = DenseTensor.__new__(DenseTensor)._init_raw(part.indices, part.data.contiguous().clone())
+            else:
+                _lib.check(_lib.load().tnc_axpy(total.dtype_code, total.size, part.data.contiguous().data_ptr(),
+                                                total.data.data_ptr(), _lib.stream_ptr()))
+        return total
+
+    def finish(self, total: DenseTensor) -> DenseTensor:
+        if self.output_order is None:
+            return total
+        by = {ix.label: ix for ix in total.indices}
+        return permute(total, [by[l] for l in self.output_order])
 
 
 class SliceExecutor:

@@ -329,3 +329,38 @@ def test_slice_executor_per_slice_roots(cuda_ready):
 
     got = permute(total, [by[l] for l in labels0]).numpy()
     assert rel_l2(got, want) <= TOL_C64
+
+
+def test_open_output_spindle_reuse(cuda_ready):
+    """Open-output reuse programs (extension of run_reuse): the spindle program
+    over the golden open network's slice spec sums to the same tensor as the
+    reference's per-slice roots, with fewer multiplies than plain slicing."""
+    from paper_2504_09186_b200 import (
+        SliceSpec, choose_reuse_subset, circuit_to_network, greedy_path, parse_circuit, plan_spindle,
+        tree_metrics,
+    )
+    from paper_2504_09186_b200.execute import run_reuse_open
+
+    g = load_golden("sliced")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits, open_qubits=g["open"])
+    t = greedy_path(net, 0)
+    spec = SliceSpec.from_json(json.dumps(g["open_net"]["slice_spec"]))
+    part = choose_reuse_subset(t, spec, None, 12)
+    rs, rep = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    labels0 = g["open_net"]["per_slice"][0]["labels"]
+    got = run_reuse_open(net, t, rs, labels0, "single").numpy()
+    want = sum(arr(it["data"]).astype(np.complex128) for it in g["open_net"]["per_slice"])
+    assert rel_l2(got, want) <= TOL_C64
+    sliced = tree_metrics(t, spec.dims_projected()).total_cost * spec.n_subtasks
+    assert rep.predicted_multiplies <= sliced
+    # the bench scheduler: same programs over the slice-invariant cache, with
+    # 3 nested labels (2^6 outer programs of 8 slices each)
+    from paper_2504_09186_b200.execute import ReuseRunner
+
+    part = choose_reuse_subset(t, spec, None, 3)
+    rs, _ = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    rr = ReuseRunner(net, rs, "single", labels0)
+    assert rr.n_programs * rr.slices_per_program == spec.n_subtasks
+    got = rr.finish(rr.run(range(rr.n_programs))).numpy()
+    assert rel_l2(got, want) <= TOL_C64
