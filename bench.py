@@ -462,6 +462,7 @@ def bench_c1(args) -> None:
     import torch
 
     from paper_2504_09186_b200 import DenseTensor, Index, _lib, contract_pair
+    from paper_2504_09186_b200.errors import TncError
     from paper_2504_09186_b200.workloads import c1_cases
 
     torch.cuda.set_device(0)
@@ -472,14 +473,19 @@ def bench_c1(args) -> None:
         da, db = case.data()
         a, b = DenseTensor(ia, da), DenseTensor(ib, db)
         del da, db
+        try:
+            contract_pair(a, b, out_order=io, variant=args.variant)
+        except TncError as exc:  # forced variant outside this shape's envelope
+            print(json.dumps({"metric": f"{case.name} contract+permute", "skipped": str(exc)}), flush=True)
+            continue
         for _ in range(args.warmup):
-            contract_pair(a, b, out_order=io)
+            contract_pair(a, b, out_order=io, variant=args.variant)
         torch.cuda.synchronize()
         lib.tnc_profile_enable(1)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(args.steps):
-            out = contract_pair(a, b, out_order=io)
+            out = contract_pair(a, b, out_order=io, variant=args.variant)
         e.record()
         e.synchronize()
         prof = _read_prof(lib)
@@ -512,7 +518,7 @@ def _read_prof(lib) -> dict:
     import ctypes
 
     out = {}
-    for kind, name in enumerate(["tc_gemm", "simt_gemm", "permute", "split_prep", "reduce", "absorb", "axpy", "stream"]):
+    for kind, name in enumerate(["tc_gemm", "simt_gemm", "permute", "split_prep", "reduce", "absorb", "axpy", "stream", "tc_gather"]):
         n = ctypes.c_int64()
         ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         lib.tnc_profile_read(kind, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by))
@@ -528,6 +534,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c2", "c1"])
     ap.add_argument("--slices-per-step", type=int, default=1)
+    ap.add_argument("--variant", type=int, default=0, help="c1: force a kernel variant (tnc_variant)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cap", type=int, default=26)
     ap.add_argument("--ref-cap", type=int, default=25)

@@ -67,9 +67,14 @@ typedef enum tnc_variant {
   TNC_VARIANT_SPLITK = 3,      /* CUDA-core split-K, fixed-order tree (tiny M*N)  */
   TNC_VARIANT_TC3XF16 = 4,     /* tcgen05 kind::f16, 2-piece FP16 split with
                                   per-row power-of-two scaling, TMEM accum        */
-  TNC_VARIANT_STREAM = 5       /* narrow step: X streamed once in place, small Y
+  TNC_VARIANT_STREAM = 5,      /* narrow step: X streamed once in place, small Y
                                   on chip, C written in the final order (c64,
                                   extent-2 legs, rows_y * K <= 4096)              */
+  TNC_VARIANT_TCGATHER = 6     /* gather-fed tcgen05 GEMM: both operands gathered
+                                  from their own layouts by the kernel, split to
+                                  3xTF32 in shared memory, split-K over CTAs; C
+                                  in the final order (c64, extent-2 legs,
+                                  rows_y <= 128, K >= 16, rows_x >= 64)           */
 } tnc_variant;
 
 /* A labeled operand: leg i has label id labels[i], extent dims[i], element

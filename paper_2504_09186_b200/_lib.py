@@ -17,7 +17,7 @@ from .errors import DeviceError, raise_for_status
 MAX_RANK = 64
 C64, C128 = 0, 1
 VARIANT_AUTO, VARIANT_SIMT, VARIANT_TC3XTF32, VARIANT_SPLITK = 0, 1, 2, 3
-VARIANT_TC3XF16, VARIANT_STREAM = 4, 5
+VARIANT_TC3XF16, VARIANT_STREAM, VARIANT_TCGATHER = 4, 5, 6
 
 _LIB_PATH = Path(__file__).resolve().parent / "libtnc_b200.so"
 

@@ -11,6 +11,7 @@ when any source is newer than the library.
 from __future__ import annotations
 
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -40,11 +41,25 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
+_INCLUDE_RE = re.compile(r'^\s*#\s*include\s*"([^"]+)"', re.M)
+
+
+def _deps(src: Path, seen: set[Path] | None = None) -> set[Path]:
+    """The source plus every local header it includes (transitively)."""
+    seen = set() if seen is None else seen
+    if src in seen or not src.exists():
+        return seen
+    seen.add(src)
+    for name in _INCLUDE_RE.findall(src.read_text(errors="ignore")):
+        _deps((src.parent / name).resolve(), seen)
+    return seen
+
+
 def _stale() -> bool:
     if not LIB.exists():
         return True
     lib_t = LIB.stat().st_mtime
-    deps = list(sources()) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+    deps = set().union(*(_deps(s) for s in sources()))
     return any(p.stat().st_mtime > lib_t for p in deps)
 
 
@@ -53,11 +68,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     OBJ.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
-    deps_t = max(p.stat().st_mtime for p in list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")))
-
     def compile_one(src: Path) -> Path:
         obj = OBJ / (src.stem + ".o")
-        if not force and obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, deps_t):
+        deps_t = max(p.stat().st_mtime for p in _deps(src))
+        if not force and obj.exists() and obj.stat().st_mtime > deps_t:
             return obj
         cmd = [cc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", "-c", str(src), "-o", str(obj)]
         if verbose:

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "tnc_common.cuh"
+#include "tnc_gather_tc.cuh"
 
 namespace tnc {
 
@@ -107,6 +108,7 @@ struct tnc_plan {
   size_t off_x, off_y, off_planes, off_partials, off_tmp, ws_bytes;
   size_t ws_layout;  // bytes of the staged-operand layout (split path); == ws_bytes unless streaming
   tnc::StreamPlan* stream = nullptr;  // TNC_VARIANT_STREAM
+  tnc::GatherTcPlan* gt = nullptr;    // TNC_VARIANT_TCGATHER
   int32_t k_splits;
   __int128 multiplies;
   // split-K with in-kernel gather (no operand permutation): packed offset
@@ -122,6 +124,7 @@ struct tnc_plan {
   ~tnc_plan() {
     if (g_dev) cudaFree(g_dev);
     if (stream) tnc::stream_destroy(stream);
+    if (gt) tnc::gather_tc_destroy(gt);
   }
 };
 
@@ -312,6 +315,60 @@ int try_stream(tnc_plan* p, const std::vector<Leg>& free_a, const std::vector<Le
   for (const Leg& l : Y.free)
     if (l.dim == 2) legs.push_back({2, 0, l.stride, out_stride(l.label)});
   return stream_prepare(static_cast<int>(legs.size()), legs.data(), &p->stream);
+}
+
+// Final output stride of every free leg (the caller's order when given).
+std::vector<std::pair<int32_t, int64_t>> final_out_strides(const tnc_plan* p, const std::vector<Leg>& free_a,
+                                                           const std::vector<Leg>& free_b) {
+  std::vector<Leg> order;
+  if (p->custom_out) {
+    std::vector<Leg> def_out = free_a;
+    def_out.insert(def_out.end(), free_b.begin(), free_b.end());
+    for (int32_t i : p->out_perm) order.push_back(def_out[i]);
+  } else {
+    order = free_a;
+    order.insert(order.end(), free_b.begin(), free_b.end());
+  }
+  std::vector<std::pair<int32_t, int64_t>> out;
+  int64_t s = 1;
+  for (int i = static_cast<int>(order.size()) - 1; i >= 0; --i) {
+    out.push_back({order[i].label, s});
+    s *= order[i].dim;
+  }
+  return out;
+}
+
+// K6 gather-fed tensor-core path: c64, every leg of extent <= 2, rows_y <= 128,
+// rows_x >= 64, K >= one k-block.  Both operands are read in place.
+int try_gather_tc(tnc_plan* p, const std::vector<Leg>& free_a, const std::vector<Leg>& free_b) {
+  if (p->dtype != TNC_C64) return TNC_ERR_UNSUPPORTED;
+  const Operand& X = p->x;
+  const Operand& Y = p->y;
+  for (const auto* v : {&X.free, &X.common, &Y.free, &Y.common})
+    for (const Leg& l : *v)
+      if (l.dim != 1 && l.dim != 2) return TNC_ERR_UNSUPPORTED;
+  const auto outs = final_out_strides(p, free_a, free_b);
+  auto out_stride = [&](int32_t label) {
+    for (auto& o : outs)
+      if (o.first == label) return o.second;
+    return static_cast<int64_t>(-1);
+  };
+  std::vector<GatherTcLeg> legs;
+  int64_t canon = 1;  // Y-free legs: canonical column index, last leg fastest
+  for (int i = static_cast<int>(Y.free.size()) - 1; i >= 0; --i) {
+    const Leg& l = Y.free[i];
+    if (l.dim == 2) legs.push_back({2, 0, l.stride, out_stride(l.label), canon});
+    canon *= l.dim;
+  }
+  canon = p->rows_y;  // X-free legs: canonical row index times rows_y
+  for (int i = static_cast<int>(X.free.size()) - 1; i >= 0; --i) {
+    const Leg& l = X.free[i];
+    if (l.dim == 2) legs.push_back({0, l.stride, 0, out_stride(l.label), canon});
+    canon *= l.dim;
+  }
+  for (size_t i = 0; i < X.common.size(); ++i)
+    if (X.common[i].dim == 2) legs.push_back({1, X.common[i].stride, Y.common[i].stride, 0, 0});
+  return gather_tc_prepare(static_cast<int>(legs.size()), legs.data(), &p->gt);
 }
 
 bool tc_eligible(const tnc_plan* p) {
@@ -550,6 +607,13 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
       return st;
     }
   }
+  if (want == TNC_VARIANT_TCGATHER) {
+    const int st = try_gather_tc(p, free_a, free_b);
+    if (st != TNC_OK) {
+      delete p;
+      return st;
+    }
+  }
   p->variant = want;
   if (want == TNC_VARIANT_SPLITK && build_gather_splitk(p)) {
     X.in_place = Y.in_place = true;  // the kernel gathers from the original strides
@@ -573,11 +637,12 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   // workspace
   const size_t eb = elem_bytes(p->dtype);
+  const bool kernel_gathers = want == TNC_VARIANT_TCGATHER;  // operands read in place
   size_t off = 0;
   p->off_x = off;
-  if (!X.in_place) off = align_up(off + static_cast<size_t>(p->rows_x) * k * eb);
+  if (!X.in_place && !kernel_gathers) off = align_up(off + static_cast<size_t>(p->rows_x) * k * eb);
   p->off_y = off;
-  if (!Y.in_place) off = align_up(off + static_cast<size_t>(p->rows_y) * k * eb);
+  if (!Y.in_place && !kernel_gathers) off = align_up(off + static_cast<size_t>(p->rows_y) * k * eb);
   p->off_planes = off;
   if (tc) {
     const size_t pe = p->variant == TNC_VARIANT_TC3XF16 ? 2 : 4;
@@ -588,12 +653,15 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   p->off_partials = off;
   if (p->k_splits > 1) off = align_up(off + static_cast<size_t>(p->k_splits) * m * n * 8);
+  if (kernel_gathers && gather_tc_splits(p->gt) > 1)
+    off = align_up(off + static_cast<size_t>(gather_tc_splits(p->gt)) * m * n * 8);
   if (p->variant == TNC_VARIANT_SPLITK) {
     const int64_t chunks = p->gather_splitk ? p->g_chunks : splitk_chunks(p->rows_x, p->rows_y, k);
     off = align_up(off + static_cast<size_t>(chunks) * m * n * eb);
   }
   p->off_tmp = off;
-  if (p->custom_out) off = align_up(off + static_cast<size_t>(m) * n * eb);
+  if (p->custom_out && !(kernel_gathers && gather_tc_splits(p->gt) == 1))
+    off = align_up(off + static_cast<size_t>(m) * n * eb);
   p->ws_bytes = off;
   p->ws_layout = off;
   if (want == TNC_VARIANT_STREAM) p->ws_bytes = 0;  // reads A/B in place, writes C in final order
@@ -694,6 +762,19 @@ int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void*
   const void* xsrc = p->x_is_a ? a : b;
   const void* ysrc = p->x_is_a ? b : a;
   if (p->variant == TNC_VARIANT_STREAM) return stream_launch(p->stream, xsrc, ysrc, c, st);
+  if (p->variant == TNC_VARIANT_TCGATHER) {
+    const int splits = gather_tc_splits(p->gt);
+    if (splits == 1) return gather_tc_launch(p->gt, xsrc, ysrc, c, nullptr, st);
+    void* parts = ws + p->off_partials;
+    TNC_TRY(gather_tc_launch(p->gt, xsrc, ysrc, nullptr, parts, st));
+    void* dst = p->custom_out ? static_cast<void*>(ws + p->off_tmp) : c;
+    TNC_TRY(tree_reduce_launch(TNC_C64, splits, p->rows_x * p->rows_y, parts, dst, p->rows_x, p->rows_y,
+                               p->ldcm, p->ldcn, st));
+    if (p->custom_out)
+      TNC_TRY(permute_launch(p->dtype, static_cast<int>(p->out_perm.size()), p->out_perm_dims.data(),
+                             p->out_perm_strides.data(), p->out_perm.data(), dst, c, st));
+    return TNC_OK;
+  }
   const void *xm, *ym;
   int64_t ldx, ldy;
   TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
@@ -711,6 +792,8 @@ int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void*
 int tnc_contract_split_workspace(const tnc_plan* p, int32_t blocks, int32_t group,
                                  size_t* workspace_bytes) {
   if (!p || !workspace_bytes) TNC_RET(TNC_ERR_INVALID, "null argument");
+  if (p->variant == TNC_VARIANT_TCGATHER)
+    TNC_RET(TNC_ERR_UNSUPPORTED, "split contraction needs a staged (non-gather) plan");
   if (blocks < 1 || group < 1) TNC_RET(TNC_ERR_CONTRACTION, "blocks*group_size must be positive");
   const int64_t panels = std::min<int64_t>(static_cast<int64_t>(blocks) * group, p->k);
   const size_t eb = elem_bytes(p->dtype);

@@ -88,7 +88,7 @@ struct Axis {
 // ---- optional per-kernel device timing (tnc_profile_*) ----
 enum ProfKind { PROF_TC_GEMM = 0, PROF_SIMT_GEMM = 1, PROF_PERMUTE = 2, PROF_SPLIT_PREP = 3,
                 PROF_REDUCE = 4, PROF_ABSORB = 5, PROF_AXPY = 6, PROF_STREAM = 7,
-                PROF_KINDS = 8 };
+                PROF_TC_GATHER = 8, PROF_AUX = 9, PROF_KINDS = 10 };
 // RAII: when profiling is enabled, records CUDA events around the launches
 // issued in its scope on `stream` and books `flops` / `bytes` of algorithmic
 // work to `kind`.

@@ -1,0 +1,710 @@
+// K6: gather-fed tensor-core contraction (3xTF32 on tcgen05, split-K).
+//
+// Reference op: contract_pair (contract.py:131-165) = permute A and B into
+// TTGT order (tensor.py:252-274), np.matmul, transpose -- and, for the
+// small-M/N huge-K steps, split_common_contract's panel sum
+// (contract.py:168-208).  Here the permutations never touch HBM: the
+// kernel's worker warps gather each operand tile straight from the
+// operand's own strided layout, split it into 3xTF32 big/small planes in
+// shared memory (the canonical 128-byte-swizzled K-major UMMA layout), and
+// one elected thread issues tcgen05.mma kind::tf32 into TMEM.  Every leg has
+// extent 2 (quantum-circuit networks), so every index map is a GF(2)-linear
+// function of the index bits: global offsets are sums of per-bit strides and
+// swizzled smem addresses are XORs of per-bit addresses.
+//
+//   tile     = 128 rows of X (7 X-free legs R) x all Y columns (<= 128
+//              complex, every Y-free leg) x one k-block of KBC complex K
+//              (kb common legs KL); R and KL are chosen on the host so that
+//              X, Y and the output are read / written in runs (tile bits
+//              cover each tensor's fastest legs)
+//   unit     = (m-block, k-split); persistent CTAs stride over units
+//   complex  = one real GEMM: X interleaved [M, 2K] times the expanded Y^
+//              (rows 2n = (Yr, -Yi), 2n+1 = (Yi, Yr)) gives interleaved C
+//   accuracy = chunks of 32 complex K accumulate in alternating TMEM buffers
+//              and are folded into fp32 registers (same scheme as K2)
+//   output   = one split: C written in its FINAL (caller's) leg order; more
+//              splits: fp32 partials [split][row][col] (canonical order),
+//              then the fixed-order tree reduction
+//
+// Roles (256 threads, 8 warps = 2 per SM sub-partition so each thread can
+// hold up to 255 registers): every warp gathers + splits (loads run one
+// k-block ahead of the smem stores), folds TMEM lane quadrant w % 4, column
+// half w / 4, and stores; warp 0 also owns TMEM and issues the MMAs of
+// k-block g-1 right after staging k-block g (one elected lane).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "tnc_common.cuh"
+#include "tnc_gather_tc.cuh"
+#include "tnc_tcgen05.cuh"
+
+namespace tnc {
+
+namespace {
+
+using namespace tc5;
+
+constexpr int kGtWorkers = 256;
+constexpr int kGtWorkerWarps = kGtWorkers / 32;
+constexpr int kGtThreads = kGtWorkers;  // warp 0 also issues the MMAs
+constexpr int kGtMaxBits = 12;  // tile bits per operand (7 row/col + 5 k)
+constexpr int kGtTabs = 5;      // outer tables: xm, om, cm (m-block), xk, yk (k-block)
+
+struct GtParams {
+  const float2* X;
+  const float2* Y;
+  float2* C;            // final output (splits == 1)
+  float2* parts;        // [splits][rows_x * rows_y] canonical order (splits > 1)
+  const int64_t* tabs;  // [kGtTabs][4][256] outer-index offset tables
+  int64_t m_blocks, kblocks, mn;
+  int splits, chunk_kb;
+  int nbx, nby;         // tile bits of X (rows + k) / Y (cols + k), by stride ascending
+  int rbits, fy;        // log2 tile rows / log2 Y columns
+  int64_t xg[kGtMaxBits];
+  uint32_t xs[kGtMaxBits];
+  int64_t yg[kGtMaxBits];
+  uint32_t ys[kGtMaxBits];
+  int64_t orow[7], crow[7], ocol[7];
+};
+
+template <int NMMA, int KBC, int STAGES>
+struct GtCfg {
+  static constexpr int kAtoms = KBC / 16;  // 128-byte (16 complex) K atoms per k-block
+  static constexpr int kXAtom = 128 * 128;
+  static constexpr int kYAtom = NMMA * 128;
+  static constexpr int kXPlane = kAtoms * kXAtom;
+  static constexpr int kYPlane = kAtoms * kYAtom;
+  static constexpr int kStage = 2 * kXPlane + 2 * kYPlane;
+  static constexpr int kAux = 2048;  // barriers, hi tables, output column table
+  static constexpr int kSmem = STAGES * kStage + 1024 + kAux;
+  static constexpr int kXPer = 128 * KBC / kGtWorkers;
+  static constexpr int kYPer = ((NMMA / 2) * KBC + kGtWorkers - 1) / kGtWorkers;
+  static constexpr int kHalf = NMMA / 2;
+  static constexpr uint32_t kIdesc = idesc_f32acc(2, 128, NMMA);
+  static_assert(kSmem <= 227 * 1024, "smem budget");
+};
+
+__device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
+  return __ldg(t + (idx & 255)) + __ldg(t + 256 + ((idx >> 8) & 255)) +
+         __ldg(t + 512 + ((idx >> 16) & 255)) + __ldg(t + 768 + ((idx >> 24) & 255));
+}
+
+__device__ __forceinline__ float2 ldg_stream(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+
+__device__ __forceinline__ void split_range(const GtParams& p, int split, int64_t& lo, int64_t& hi) {
+  lo = p.kblocks * split / p.splits;
+  hi = p.kblocks * (split + 1) / p.splits;
+}
+
+// Unit / k-block cursor over this CTA's share of the (m-block, split) units.
+struct GtCursor {
+  int64_t u, kb, kb_hi;
+  __device__ __forceinline__ void open(const GtParams& p, int64_t units) {
+    if (u < units) split_range(p, static_cast<int>(u % p.splits), kb, kb_hi);
+  }
+  // advance one k-block; true when a new unit was entered
+  __device__ __forceinline__ bool next(const GtParams& p, int64_t units) {
+    if (++kb < kb_hi) return false;
+    u += gridDim.x;
+    open(p, units);
+    return true;
+  }
+};
+
+template <int NMMA, int KBC, int STAGES>
+__global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
+  using Cfg = GtCfg<NMMA, KBC, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* aux = smem + STAGES * Cfg::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int64_t* xhi_g = reinterpret_cast<int64_t*>(aux + 256);  // [16]
+  int64_t* yhi_g = xhi_g + 16;                              // [16]
+  uint32_t* xhi_s = reinterpret_cast<uint32_t*>(yhi_g + 16);
+  uint32_t* yhi_s = xhi_s + 16;
+  int64_t* ocol_t = reinterpret_cast<int64_t*>(aux + 1024);  // [128] output offset of column n
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int t = threadIdx.x;
+  const int64_t units = p.m_blocks * p.splits;
+
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kGtWorkers);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kGtWorkerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (t < 16) {
+    int64_t g = 0, h = 0;
+    uint32_t s = 0, q = 0;
+    for (int j = 8; j < p.nbx; ++j)
+      if ((t >> (j - 8)) & 1) {
+        g += p.xg[j];
+        s ^= p.xs[j];
+      }
+    for (int j = 8; j < p.nby; ++j)
+      if ((t >> (j - 8)) & 1) {
+        h += p.yg[j];
+        q ^= p.ys[j];
+      }
+    xhi_g[t] = g;
+    xhi_s[t] = s;
+    yhi_g[t] = h;
+    yhi_s[t] = q;
+  }
+  if (t < 128) {
+    int64_t o = 0;
+    for (int j = 0; j < p.fy; ++j)
+      if ((t >> j) & 1) o += p.ocol[j];
+    ocol_t[t] = o;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(static_cast<uint32_t>(2 * NMMA)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t smem0 = smem_u32(smem);
+
+  const int quad = warp & 3;
+  const int half = warp >> 2;
+  int64_t xg_lo = 0, yg_lo = 0;
+  uint32_t xs_lo = 0, ys_lo = 0;
+  for (int j = 0; j < 8; ++j) {
+    if ((t >> j) & 1) {
+      if (j < p.nbx) {
+        xg_lo += p.xg[j];
+        xs_lo ^= p.xs[j];
+      }
+      if (j < p.nby) {
+        yg_lo += p.yg[j];
+        ys_lo ^= p.ys[j];
+      }
+    }
+  }
+  const int x_iters = p.nbx > 8 ? (1 << (p.nbx - 8)) : 1;
+  const bool x_act = t < (1 << p.nbx);
+  const int y_iters = p.nby > 8 ? (1 << (p.nby - 8)) : 1;
+  const bool y_act = t < (1 << p.nby);
+
+  float acc[Cfg::kHalf];
+#pragma unroll
+  for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
+
+  // producer cursor (loads run one k-block ahead of the smem stores)
+  GtCursor pc{static_cast<int64_t>(blockIdx.x), 0, 0};
+  pc.open(p, units);
+  // MMA issue cursor (warp 0 issues k-block g-1 after staging k-block g)
+  GtCursor ic{static_cast<int64_t>(blockIdx.x), 0, 0};
+  ic.open(p, units);
+  int i_in_chunk = 0;
+  uint32_t i_ch = 0, i_g = 0;
+  uint32_t dcol = 0;
+  // fold cursor (chunk sequence of this CTA's units)
+  int64_t fu = blockIdx.x, f_n = 0;
+  int f_c = 0, f_nch = 0;
+  uint32_t f_base = 0, ch = 0;
+  if (fu < units) {
+    int64_t lo, hi;
+    split_range(p, static_cast<int>(fu % p.splits), lo, hi);
+    f_n = hi - lo;
+    f_nch = static_cast<int>((f_n + p.chunk_kb - 1) / p.chunk_kb);
+  }
+
+  float2 cx[Cfg::kXPer], cy[Cfg::kYPer];
+  auto load = [&](float2 (&vx)[Cfg::kXPer], float2 (&vy)[Cfg::kYPer]) {
+    const float2* xb = p.X + tab4(p.tabs, pc.u / p.splits) + tab4(p.tabs + 3 * 1024, pc.kb) + xg_lo;
+    const float2* yb = p.Y + tab4(p.tabs + 4 * 1024, pc.kb) + yg_lo;
+#pragma unroll
+    for (int i = 0; i < Cfg::kXPer; ++i)
+      if (i < x_iters && x_act) vx[i] = ldg_stream(xb + xhi_g[i]);
+#pragma unroll
+    for (int i = 0; i < Cfg::kYPer; ++i)
+      if (i < y_iters && y_act) vy[i] = __ldg(yb + yhi_g[i]);
+  };
+  bool have = pc.u < units;
+  if (have) {
+    load(cx, cy);
+    pc.next(p, units);
+  }
+  // clock g advances once per iteration, staging or not (staged = k-blocks
+  // staged so far): the MMA issue (up to g-2) and the fold (chunks ending at
+  // or before g-3) keep their lags after staging ends, which is what frees
+  // each TMEM buffer before the MMAs that reuse it are issued
+  uint32_t g = 0, staged = 0;
+  while (true) {
+    if (have) {
+      // 1. prefetch the next k-block into registers
+      float2 nx[Cfg::kXPer], ny[Cfg::kYPer];
+      const bool have_next = pc.u < units;
+      if (have_next) {
+        load(nx, ny);
+        pc.next(p, units);
+      }
+      // 2. split the current one into 3xTF32 planes of stage g % STAGES
+      const uint32_t s = staged % STAGES;
+      mbar_wait(&empty[s], ((staged / STAGES) & 1) ^ 1);
+      const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) {
+        if (i < x_iters && x_act) {
+          const uint32_t a = st + (xs_lo ^ xhi_s[i]);
+          const float hr = tf32_rna(cx[i].x), hi = tf32_rna(cx[i].y);
+          sts2(a, hr, hi);
+          sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) {
+        if (i < y_iters && y_act) {
+          const uint32_t a0 = st + 2 * Cfg::kXPlane + (ys_lo ^ yhi_s[i]);
+          const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
+          const float hr = tf32_rna(cy[i].x), hi = tf32_rna(cy[i].y);
+          const float lr = cy[i].x - hr, li = cy[i].y - hi;
+          sts2(a0, hr, -hi);
+          sts2(a1, hi, hr);
+          sts2(a0 + Cfg::kYPlane, lr, -li);
+          sts2(a1 + Cfg::kYPlane, li, lr);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+      ++staged;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) cx[i] = nx[i];
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) cy[i] = ny[i];
+      have = have_next;
+    }
+    ++g;
+    // 3. warp 0 issues the MMAs of the staged k-blocks up to g-2
+    if (warp == 0) {
+      while (ic.u < units && i_g + 1 < g && i_g < staged) {
+        if (i_in_chunk == 0) {
+          const uint32_t b = i_ch & 1;
+          mbar_wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
+          fence_after_sync();
+          dcol = tmem_base + b * NMMA;
+        }
+        const uint32_t s = i_g % STAGES;
+        mbar_wait(&full[s], (i_g / STAGES) & 1);
+        fence_after_sync();
+        const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+        for (int a = 0; a < Cfg::kAtoms; ++a) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t xo = st + a * Cfg::kXAtom + kk * 32;
+            const uint32_t yo = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
+            const uint64_t x_big = umma_desc_sw128(xo);
+            const uint64_t x_small = umma_desc_sw128(xo + Cfg::kXPlane);
+            const uint64_t y_big = umma_desc_sw128(yo);
+            const uint64_t y_small = umma_desc_sw128(yo + Cfg::kYPlane);
+            const uint32_t acc0 = (i_in_chunk > 0 || a > 0 || kk > 0) ? 1u : 0u;
+            // small products first: accumulated before the big one
+            mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
+            mma_tf32_elect(dcol, x_big, y_small, Cfg::kIdesc, 1u);
+            mma_tf32_elect(dcol, x_big, y_big, Cfg::kIdesc, 1u);
+          }
+        }
+        mma_commit_elect(&empty[s]);
+        ++i_g;
+        const bool unit_end = ic.kb + 1 == ic.kb_hi;
+        if (++i_in_chunk == p.chunk_kb || unit_end) {
+          mma_commit_elect(&tfull[i_ch & 1]);
+          ++i_ch;
+          i_in_chunk = 0;
+        }
+        ic.next(p, units);
+      }
+    }
+    // 4. fold the chunks ending at or before g-3: their last MMAs were issued
+    //    an iteration ago and the following k-block's MMAs keep the tensor
+    //    pipe busy meanwhile
+    while (fu < units) {
+      const int64_t end = static_cast<int64_t>(f_c + 1) * p.chunk_kb;
+      const int64_t last = static_cast<int64_t>(f_base) + (end < f_n ? end : f_n) - 1;
+      if (last + 3 > static_cast<int64_t>(g)) break;
+      const uint32_t b = ch & 1;
+      mbar_wait(&tfull[b], (ch >> 1) & 1);
+      fence_after_sync();
+      const uint32_t taddr =
+          tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + b * NMMA + half * Cfg::kHalf;
+#pragma unroll
+      for (int gi = 0; gi < Cfg::kHalf / 16; ++gi) {
+        uint32_t v[16];
+        tmem_ld16(taddr + gi * 16, v);
+        tmem_wait_ld();
+        if (f_c == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[gi * 16 + j] = __uint_as_float(v[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[gi * 16 + j] += __uint_as_float(v[j]);
+        }
+      }
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      ++ch;
+      if (f_c == f_nch - 1) {
+        // unit finished: store this thread's row (one TMEM lane), its column half
+        const int r = quad * 32 + lane;
+        const int64_t mb = fu / p.splits;
+        const int split = static_cast<int>(fu % p.splits);
+        if (r < (1 << p.rbits)) {
+          const int n0 = half * (Cfg::kHalf / 2);
+          const int ncols = min(Cfg::kHalf / 2, (1 << p.fy) - n0);
+          if (p.splits == 1) {
+            int64_t base = tab4(p.tabs + 1 * 1024, mb);
+            for (int j = 0; j < p.rbits; ++j)
+              if ((r >> j) & 1) base += p.orow[j];
+#pragma unroll
+            for (int j = 0; j < Cfg::kHalf / 2; ++j)
+              if (j < ncols) p.C[base + ocol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          } else {
+            int64_t base = tab4(p.tabs + 2 * 1024, mb);
+            for (int j = 0; j < p.rbits; ++j)
+              if ((r >> j) & 1) base += p.crow[j];
+            float2* dst = p.parts + split * p.mn + base + n0;
+#pragma unroll
+            for (int j = 0; j < Cfg::kHalf / 2; ++j)
+              if (j < ncols) dst[j] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          }
+        }
+        f_base += static_cast<uint32_t>(f_n);
+        fu += gridDim.x;
+        f_c = 0;
+        if (fu < units) {
+          int64_t lo, hi;
+          split_range(p, static_cast<int>(fu % p.splits), lo, hi);
+          f_n = hi - lo;
+          f_nch = static_cast<int>((f_n + p.chunk_kb - 1) / p.chunk_kb);
+        }
+      } else {
+        ++f_c;
+      }
+    }
+    if (!have && fu >= units) break;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(static_cast<uint32_t>(2 * NMMA)));
+  }
+}
+
+}  // namespace
+
+struct GatherTcPlan {
+  GtParams p;
+  int nmma = 0, kbc = 0;
+  int64_t rows_x = 0, rows_y = 0, k = 0;
+  std::vector<int64_t> tabs_host;
+  mutable std::mutex mu;
+  mutable int64_t* tabs_dev = nullptr;
+  ~GatherTcPlan() {
+    if (tabs_dev) cudaFree(tabs_dev);
+  }
+};
+
+namespace {
+
+// 4 levels x 256 entries: T[l][v] = sum of strides[8l + b] over set bits b of v
+void build_tab4(const std::vector<int64_t>& strides, int64_t* out) {
+  for (int l = 0; l < 4; ++l)
+    for (int v = 0; v < 256; ++v) {
+      int64_t s = 0;
+      for (int b = 0; b < 8; ++b)
+        if (((v >> b) & 1) && 8 * l + b < static_cast<int>(strides.size())) s += strides[8 * l + b];
+      out[l * 256 + v] = s;
+    }
+}
+
+// Smem byte address (XOR-linear part) of one tile bit: X rows / Y^ rows of
+// 128 bytes, 16-byte chunks swizzled by (row & 7), K atoms of atom_bytes.
+uint32_t row_bit_addr(int row_bit) {
+  const uint32_t rho = 1u << row_bit;
+  return ((rho & 7u) << 4) | (rho << 7);
+}
+uint32_t k_bit_addr(int j, uint32_t atom_bytes) {
+  if (j == 0) return 1u << 3;
+  if (j <= 3) return 1u << (4 + j - 1);
+  return (1u << (j - 4)) * atom_bytes;
+}
+
+double eff(int run) { return std::min(1.0, std::ldexp(1.0, run) / 4.0) + 0.1 * std::min(1.0, std::ldexp(1.0, run) / 16.0); }
+
+}  // namespace
+
+int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
+  *out = nullptr;
+  std::vector<int> xf, cm, yf;  // indices into legs
+  for (int i = 0; i < n_legs; ++i) {
+    if (legs[i].kind == 0) xf.push_back(i);
+    else if (legs[i].kind == 1) cm.push_back(i);
+    else yf.push_back(i);
+  }
+  const int fx = static_cast<int>(xf.size()), c = static_cast<int>(cm.size()),
+            fy = static_cast<int>(yf.size());
+  if (fy > 7) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: Y has more than 128 columns");
+  if (fx < 6) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: X has fewer than 64 rows");
+  const int nmma = std::max(32, 2 << fy);
+  const int kbc = nmma <= 64 ? 32 : 16;
+  const int kb = kbc == 32 ? 5 : 4;
+  if (c < kb) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: K smaller than one k-block");
+  const int rb = std::min(7, fx);
+  if (fx - rb > 32 || c - kb > 32) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: outer index > 32 bits");
+
+  const double rows_x = std::ldexp(1.0, fx), rows_y = std::ldexp(1.0, fy), kk = std::ldexp(1.0, c);
+  const double wx = rows_x * kk, wy = rows_y * kk, wo = rows_x * rows_y;
+  std::vector<int> xo(xf), yo(cm), oo(xf);  // per-tensor stride orders
+  xo.insert(xo.end(), cm.begin(), cm.end());
+  yo.insert(yo.end(), yf.begin(), yf.end());
+  oo.insert(oo.end(), yf.begin(), yf.end());
+  std::sort(xo.begin(), xo.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::sort(yo.begin(), yo.end(), [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
+  std::sort(oo.begin(), oo.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
+  std::vector<char> inR(n_legs, 0), inK(n_legs, 0);
+  int nR = 0, nK = 0;
+  auto in_x = [&](int i) { return inR[i] || inK[i]; };
+  auto in_y = [&](int i) { return legs[i].kind == 2 || inK[i]; };
+  auto in_o = [&](int i) { return legs[i].kind == 2 || inR[i]; };
+  auto run = [&](const std::vector<int>& order, auto in) {
+    int r = 0;
+    while (r < static_cast<int>(order.size()) && in(order[r])) ++r;
+    return r;
+  };
+  auto first_missing = [&](const std::vector<int>& order, auto in) {
+    for (int i : order)
+      if (!in(i)) return i;
+    return -1;
+  };
+  // greedy: each step adds the leg that most improves the access efficiency of
+  // X reads, Y reads or output writes (weighted by their bytes)
+  while (nR < rb || nK < kb) {
+    double best = 0;
+    int pick = -1;
+    auto consider = [&](int leg, double w, const std::vector<int>& order, auto in) {
+      if (leg < 0) return;
+      const bool free_x = legs[leg].kind == 0;
+      if (free_x ? nR >= rb : nK >= kb) return;
+      const int before = run(order, in);
+      (free_x ? inR : inK)[leg] = 1;
+      const int after = run(order, in);
+      (free_x ? inR : inK)[leg] = 0;
+      const double gain = w * (eff(after) - eff(before));
+      if (gain > best) {
+        best = gain;
+        pick = leg;
+      }
+    };
+    consider(first_missing(xo, in_x), wx, xo, in_x);
+    consider(first_missing(yo, in_y), wy, yo, in_y);
+    consider(first_missing(oo, in_o), wo, oo, in_o);
+    if (pick < 0) break;
+    if (legs[pick].kind == 0) {
+      inR[pick] = 1;
+      ++nR;
+    } else {
+      inK[pick] = 1;
+      ++nK;
+    }
+  }
+  for (int i : xo) {  // fill what is left with X's fastest legs
+    if (legs[i].kind == 0 && !inR[i] && nR < rb) {
+      inR[i] = 1;
+      ++nR;
+    }
+    if (legs[i].kind == 1 && !inK[i] && nK < kb) {
+      inK[i] = 1;
+      ++nK;
+    }
+  }
+  // bit assignments
+  std::vector<int> R, KL, outer_m, outer_k, ncols(yf);
+  for (int i : xf)
+    (inR[i] ? R : outer_m).push_back(i);
+  for (int i : cm)
+    (inK[i] ? KL : outer_k).push_back(i);
+  std::sort(R.begin(), R.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
+  std::sort(KL.begin(), KL.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::sort(outer_m.begin(), outer_m.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::sort(outer_k.begin(), outer_k.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::sort(ncols.begin(), ncols.end(), [&](int a, int b) { return legs[a].canon_stride < legs[b].canon_stride; });
+
+  auto* plan = new GatherTcPlan();
+  std::memset(&plan->p, 0, sizeof(plan->p));
+  GtParams& p = plan->p;
+  plan->nmma = nmma;
+  plan->kbc = kbc;
+  plan->rows_x = int64_t{1} << fx;
+  plan->rows_y = int64_t{1} << fy;
+  plan->k = int64_t{1} << c;
+  p.rbits = rb;
+  p.fy = fy;
+  const uint32_t xatom = 128 * 128, yatom = static_cast<uint32_t>(nmma) * 128;
+  auto pos = [](const std::vector<int>& v, int leg) {
+    return static_cast<int>(std::find(v.begin(), v.end(), leg) - v.begin());
+  };
+  {  // X tile bits by X stride
+    std::vector<int> bits(R);
+    bits.insert(bits.end(), KL.begin(), KL.end());
+    std::sort(bits.begin(), bits.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+    p.nbx = static_cast<int>(bits.size());
+    for (int j = 0; j < p.nbx; ++j) {
+      const int leg = bits[j];
+      p.xg[j] = legs[leg].x_stride;
+      p.xs[j] = legs[leg].kind == 0 ? row_bit_addr(pos(R, leg)) : k_bit_addr(pos(KL, leg), xatom);
+    }
+  }
+  {  // Y tile bits by Y stride; column n bit j <-> ncols[j], Y^ row 2n
+    std::vector<int> bits(ncols);
+    bits.insert(bits.end(), KL.begin(), KL.end());
+    std::sort(bits.begin(), bits.end(), [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
+    p.nby = static_cast<int>(bits.size());
+    for (int j = 0; j < p.nby; ++j) {
+      const int leg = bits[j];
+      p.yg[j] = legs[leg].y_stride;
+      p.ys[j] = legs[leg].kind == 2 ? row_bit_addr(pos(ncols, leg) + 1) : k_bit_addr(pos(KL, leg), yatom);
+    }
+  }
+  for (int j = 0; j < rb; ++j) {
+    p.orow[j] = legs[R[j]].out_stride;
+    p.crow[j] = legs[R[j]].canon_stride;
+  }
+  for (int j = 0; j < fy; ++j) p.ocol[j] = legs[ncols[j]].out_stride;
+  p.m_blocks = int64_t{1} << (fx - rb);
+  p.kblocks = int64_t{1} << (c - kb);
+  p.mn = plan->rows_x * plan->rows_y;
+  // outer tables
+  plan->tabs_host.assign(static_cast<size_t>(kGtTabs) * 1024, 0);
+  std::vector<int64_t> sxm, som, scm, sxk, syk;
+  for (int i : outer_m) {
+    sxm.push_back(legs[i].x_stride);
+    som.push_back(legs[i].out_stride);
+    scm.push_back(legs[i].canon_stride);
+  }
+  for (int i : outer_k) {
+    sxk.push_back(legs[i].x_stride);
+    syk.push_back(legs[i].y_stride);
+  }
+  build_tab4(sxm, plan->tabs_host.data() + 0 * 1024);
+  build_tab4(som, plan->tabs_host.data() + 1 * 1024);
+  build_tab4(scm, plan->tabs_host.data() + 2 * 1024);
+  build_tab4(sxk, plan->tabs_host.data() + 3 * 1024);
+  build_tab4(syk, plan->tabs_host.data() + 4 * 1024);
+  // k-splits: enough units for every SM, each SM's share within ~3% of the others
+  const int sms = num_sms();
+  int splits = 1;
+  if (p.m_blocks < 4 * sms) {
+    double best_eff = 0;
+    const int64_t smax = std::min<int64_t>(p.kblocks, 4096);
+    for (int64_t s = 1; s <= smax; ++s) {
+      const int64_t units = p.m_blocks * s;
+      const double e = static_cast<double>(units) / (ceil_div(units, sms) * sms);
+      if (e > best_eff + 1e-9) {
+        best_eff = e;
+        splits = static_cast<int>(s);
+      }
+      if (units >= sms && e >= 0.97) break;
+    }
+  }
+  if (const char* env = std::getenv("TNC_GT_SPLITS")) {
+    const int64_t forced = std::atoll(env);
+    if (forced >= 1) splits = static_cast<int>(std::min<int64_t>(forced, p.kblocks));
+  }
+  p.splits = splits;
+  p.chunk_kb = std::max(1, 32 / kbc);
+  if (const char* env = std::getenv("TNC_GT_CHUNK")) p.chunk_kb = std::max(1, std::atoi(env));
+  *out = plan;
+  return TNC_OK;
+}
+
+int gather_tc_splits(const GatherTcPlan* plan) { return plan->p.splits; }
+
+void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
+
+namespace {
+
+template <int NMMA, int KBC, int STAGES>
+int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
+  using Cfg = GtCfg<NMMA, KBC, STAGES>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES>;
+  TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+  const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
+  ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
+  kern<<<grid, kGtThreads, Cfg::kSmem, stream>>>(p);
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+}  // namespace
+
+int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, void* c_final, void* parts,
+                     cudaStream_t stream) {
+  {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (!plan->tabs_dev) {
+      const size_t bytes = plan->tabs_host.size() * sizeof(int64_t);
+      TNC_CUDA_TRY(cudaMalloc(&plan->tabs_dev, bytes));
+      TNC_CUDA_TRY(cudaMemcpy(plan->tabs_dev, plan->tabs_host.data(), bytes, cudaMemcpyHostToDevice));
+    }
+  }
+  GtParams p = plan->p;
+  p.X = static_cast<const float2*>(x);
+  p.Y = static_cast<const float2*>(y);
+  p.C = static_cast<float2*>(c_final);
+  p.parts = static_cast<float2*>(parts);
+  p.tabs = plan->tabs_dev;
+  if (p.splits == 1 && !p.C) TNC_RET(TNC_ERR_INVALID, "tc_gather: null output");
+  if (p.splits > 1 && !p.parts) TNC_RET(TNC_ERR_INVALID, "tc_gather: null partials");
+  const int64_t units = p.m_blocks * p.splits;
+  const double M = static_cast<double>(plan->rows_x), N = static_cast<double>(plan->rows_y),
+               K = static_cast<double>(plan->k);
+  const double flops = 8.0 * M * N * K, bytes = 8.0 * (M * K + N * K + M * N);
+  switch (plan->nmma) {
+    case 32: return launch_gt<32, 32, 2>(p, units, flops, bytes, stream);
+    case 64: return launch_gt<64, 32, 2>(p, units, flops, bytes, stream);
+    case 128: return launch_gt<128, 16, 3>(p, units, flops, bytes, stream);
+    case 256: return launch_gt<256, 16, 2>(p, units, flops, bytes, stream);
+    default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
+  }
+}
+
+}  // namespace tnc
