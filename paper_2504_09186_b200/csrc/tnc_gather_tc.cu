@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -50,8 +51,8 @@ using namespace tc5;
 constexpr int kGtWorkers = 256;
 constexpr int kGtWorkerWarps = kGtWorkers / 32;
 constexpr int kGtThreads = kGtWorkers;  // warp 0 also issues the MMAs
-constexpr int kGtMaxBits = 12;  // tile bits per operand (7 row/col + 5 k)
-constexpr int kGtTabs = 5;      // outer tables: xm, om, cm (m-block), xk, yk (k-block)
+constexpr int kGtMaxBits = 12;          // tile bits per operand (7 row/col + 5 k)
+constexpr int kGtTabs = 5;              // outer tables: xm, om, cm (m-block), xk, yk (k-block)
 
 struct GtParams {
   const float2* X;
@@ -61,30 +62,35 @@ struct GtParams {
   const int64_t* tabs;  // [kGtTabs][4][256] outer-index offset tables
   int64_t m_blocks, kblocks, mn;
   int splits, chunk_kb;
-  int nbx, nby;         // tile bits of X (rows + k) / Y (cols + k), by stride ascending
-  int rbits, fy;        // log2 tile rows / log2 Y columns
-  int64_t xg[kGtMaxBits];
-  uint32_t xs[kGtMaxBits];
-  int64_t yg[kGtMaxBits];
-  uint32_t ys[kGtMaxBits];
-  int64_t orow[7], crow[7], ocol[7];
+  int rbits, fy;        // real row / column bits (phantom bits, stride 0, sit above)
+  // tile bit j (thread bit j for j < 8, iteration bit j - 8 above): element
+  // offset in the operand and XOR-linear smem byte address in the stage plane
+  uint32_t xg[kGtMaxBits], xs[kGtMaxBits];
+  uint32_t yg[kGtMaxBits], ys[kGtMaxBits];
+  int64_t orow[7], crow[7];  // per tile-row bit: final / partial-layout stride
+  int64_t ocol[7], ccol[7];  // per column bit
 };
 
 template <int NMMA, int KBC, int STAGES>
 struct GtCfg {
-  static constexpr int kAtoms = KBC / 16;  // 128-byte (16 complex) K atoms per k-block
+  static constexpr int kLogK = KBC == 32 ? 5 : 4;
+  static constexpr int kLogN = NMMA == 32 ? 4 : NMMA == 64 ? 5 : NMMA == 128 ? 6 : 7;  // log2(NMMA / 2)
+  static constexpr int kXBits = 7 + kLogK;
+  static constexpr int kYBits = kLogN + kLogK;
+  static constexpr int kXPer = 1 << (kXBits - 8);  // X elements per thread per k-block
+  static constexpr int kYPer = 1 << (kYBits - 8);
+  static constexpr bool kPre = NMMA <= 128;       // per-thread offsets kept in registers
+  static constexpr int kAtoms = KBC / 16;         // 128-byte (16 complex) K atoms per k-block
   static constexpr int kXAtom = 128 * 128;
   static constexpr int kYAtom = NMMA * 128;
   static constexpr int kXPlane = kAtoms * kXAtom;
   static constexpr int kYPlane = kAtoms * kYAtom;
   static constexpr int kStage = 2 * kXPlane + 2 * kYPlane;
-  static constexpr int kAux = 2048;  // barriers, hi tables, output column table
-  static constexpr int kSmem = STAGES * kStage + 1024 + kAux;
-  static constexpr int kXPer = 128 * KBC / kGtWorkers;
-  static constexpr int kYPer = ((NMMA / 2) * KBC + kGtWorkers - 1) / kGtWorkers;
+  static constexpr int kSmem = STAGES * kStage + 1024;
   static constexpr int kHalf = NMMA / 2;
   static constexpr uint32_t kIdesc = idesc_f32acc(2, 128, NMMA);
-  static_assert(kSmem <= 227 * 1024, "smem budget");
+  static_assert(kSmem + 4096 <= 227 * 1024, "smem budget");
+  static_assert(kXBits >= 8 && kYBits >= 8, "tile smaller than the CTA");
 };
 
 __device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
@@ -100,10 +106,10 @@ __device__ __forceinline__ float2 ldg_stream(const float2* p) {
   return v;
 }
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// TF32 "big" part, round-half-away on the 13 dropped mantissa bits (two
+// integer ops; the tensor core reads only the top 19 bits of each fp32)
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
@@ -121,12 +127,10 @@ struct GtCursor {
   __device__ __forceinline__ void open(const GtParams& p, int64_t units) {
     if (u < units) split_range(p, static_cast<int>(u % p.splits), kb, kb_hi);
   }
-  // advance one k-block; true when a new unit was entered
-  __device__ __forceinline__ bool next(const GtParams& p, int64_t units) {
-    if (++kb < kb_hi) return false;
+  __device__ __forceinline__ void next(const GtParams& p, int64_t units) {
+    if (++kb < kb_hi) return;
     u += gridDim.x;
     open(p, units);
-    return true;
   }
 };
 
@@ -134,20 +138,12 @@ template <int NMMA, int KBC, int STAGES>
 __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
   using Cfg = GtCfg<NMMA, KBC, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t xhi_g[16], xhi_s[16], yhi_g[16], yhi_s[16];
+  __shared__ int64_t ocol_t[128], ccol_t[128];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* aux = smem + STAGES * Cfg::kStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int64_t* xhi_g = reinterpret_cast<int64_t*>(aux + 256);  // [16]
-  int64_t* yhi_g = xhi_g + 16;                              // [16]
-  uint32_t* xhi_s = reinterpret_cast<uint32_t*>(yhi_g + 16);
-  uint32_t* yhi_s = xhi_s + 16;
-  int64_t* ocol_t = reinterpret_cast<int64_t*>(aux + 1024);  // [128] output offset of column n
-
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int t = threadIdx.x;
@@ -165,14 +161,13 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (t < 16) {
-    int64_t g = 0, h = 0;
-    uint32_t s = 0, q = 0;
-    for (int j = 8; j < p.nbx; ++j)
+    uint32_t g = 0, s = 0, h = 0, q = 0;
+    for (int j = 8; j < Cfg::kXBits; ++j)
       if ((t >> (j - 8)) & 1) {
         g += p.xg[j];
         s ^= p.xs[j];
       }
-    for (int j = 8; j < p.nby; ++j)
+    for (int j = 8; j < Cfg::kYBits; ++j)
       if ((t >> (j - 8)) & 1) {
         h += p.yg[j];
         q ^= p.ys[j];
@@ -183,59 +178,70 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     yhi_s[t] = q;
   }
   if (t < 128) {
-    int64_t o = 0;
+    int64_t o = 0, c = 0;
     for (int j = 0; j < p.fy; ++j)
-      if ((t >> j) & 1) o += p.ocol[j];
+      if ((t >> j) & 1) {
+        o += p.ocol[j];
+        c += p.ccol[j];
+      }
     ocol_t[t] = o;
+    ccol_t[t] = c;
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
+                     smem_u32(&tmem_slot)),
                  "r"(static_cast<uint32_t>(2 * NMMA)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = tmem_slot;
   const uint32_t smem0 = smem_u32(smem);
 
   const int quad = warp & 3;
   const int half = warp >> 2;
-  int64_t xg_lo = 0, yg_lo = 0;
-  uint32_t xs_lo = 0, ys_lo = 0;
+  uint32_t xg_lo = 0, yg_lo = 0, xs_lo = 0, ys_lo = 0;
+#pragma unroll
   for (int j = 0; j < 8; ++j) {
     if ((t >> j) & 1) {
-      if (j < p.nbx) {
-        xg_lo += p.xg[j];
-        xs_lo ^= p.xs[j];
-      }
-      if (j < p.nby) {
-        yg_lo += p.yg[j];
-        ys_lo ^= p.ys[j];
-      }
+      xg_lo += p.xg[j];
+      xs_lo ^= p.xs[j];
+      yg_lo += p.yg[j];
+      ys_lo ^= p.ys[j];
     }
   }
-  const int x_iters = p.nbx > 8 ? (1 << (p.nbx - 8)) : 1;
-  const bool x_act = t < (1 << p.nbx);
-  const int y_iters = p.nby > 8 ? (1 << (p.nby - 8)) : 1;
-  const bool y_act = t < (1 << p.nby);
+  // per-thread element offsets / smem addresses of its tile elements
+  uint32_t xo[Cfg::kPre ? Cfg::kXPer : 1], xa[Cfg::kPre ? Cfg::kXPer : 1];
+  uint32_t yo[Cfg::kPre ? Cfg::kYPer : 1], ya[Cfg::kPre ? Cfg::kYPer : 1];
+  if constexpr (Cfg::kPre) {
+#pragma unroll
+    for (int i = 0; i < Cfg::kXPer; ++i) {
+      xo[i] = xg_lo + xhi_g[i];
+      xa[i] = xs_lo ^ xhi_s[i];
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::kYPer; ++i) {
+      yo[i] = yg_lo + yhi_g[i];
+      ya[i] = ys_lo ^ yhi_s[i];
+    }
+  }
+  auto xoff = [&](int i) { if constexpr (Cfg::kPre) return xo[i]; else return xg_lo + xhi_g[i]; };
+  auto xadr = [&](int i) { if constexpr (Cfg::kPre) return xa[i]; else return xs_lo ^ xhi_s[i]; };
+  auto yoff = [&](int i) { if constexpr (Cfg::kPre) return yo[i]; else return yg_lo + yhi_g[i]; };
+  auto yadr = [&](int i) { if constexpr (Cfg::kPre) return ya[i]; else return ys_lo ^ yhi_s[i]; };
 
   float acc[Cfg::kHalf];
 #pragma unroll
   for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
 
-  // producer cursor (loads run one k-block ahead of the smem stores)
-  GtCursor pc{static_cast<int64_t>(blockIdx.x), 0, 0};
+  GtCursor pc{static_cast<int64_t>(blockIdx.x), 0, 0};  // loads (one k-block ahead)
   pc.open(p, units);
-  // MMA issue cursor (warp 0 issues k-block g-1 after staging k-block g)
-  GtCursor ic{static_cast<int64_t>(blockIdx.x), 0, 0};
+  GtCursor ic{static_cast<int64_t>(blockIdx.x), 0, 0};  // MMA issue (warp 0)
   ic.open(p, units);
   int i_in_chunk = 0;
-  uint32_t i_ch = 0, i_g = 0;
-  uint32_t dcol = 0;
-  // fold cursor (chunk sequence of this CTA's units)
-  int64_t fu = blockIdx.x, f_n = 0;
+  uint32_t i_ch = 0, i_g = 0, dcol = 0;
+  int64_t fu = blockIdx.x, f_n = 0;  // fold cursor over this CTA's chunk sequence
   int f_c = 0, f_nch = 0;
   uint32_t f_base = 0, ch = 0;
   if (fu < units) {
@@ -247,73 +253,41 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 
   float2 cx[Cfg::kXPer], cy[Cfg::kYPer];
   auto load = [&](float2 (&vx)[Cfg::kXPer], float2 (&vy)[Cfg::kYPer]) {
-    const float2* xb = p.X + tab4(p.tabs, pc.u / p.splits) + tab4(p.tabs + 3 * 1024, pc.kb) + xg_lo;
-    const float2* yb = p.Y + tab4(p.tabs + 4 * 1024, pc.kb) + yg_lo;
+    const float2* xb = p.X + (tab4(p.tabs, pc.u / p.splits) + tab4(p.tabs + 3 * 1024, pc.kb));
+    const float2* yb = p.Y + tab4(p.tabs + 4 * 1024, pc.kb);
 #pragma unroll
-    for (int i = 0; i < Cfg::kXPer; ++i)
-      if (i < x_iters && x_act) vx[i] = ldg_stream(xb + xhi_g[i]);
+    for (int i = 0; i < Cfg::kXPer; ++i) vx[i] = ldg_stream(xb + xoff(i));
 #pragma unroll
-    for (int i = 0; i < Cfg::kYPer; ++i)
-      if (i < y_iters && y_act) vy[i] = __ldg(yb + yhi_g[i]);
+    for (int i = 0; i < Cfg::kYPer; ++i) vy[i] = __ldg(yb + yoff(i));
   };
   bool have = pc.u < units;
   if (have) {
     load(cx, cy);
     pc.next(p, units);
   }
-  // clock g advances once per iteration, staging or not (staged = k-blocks
-  // staged so far): the MMA issue (up to g-2) and the fold (chunks ending at
-  // or before g-3) keep their lags after staging ends, which is what frees
-  // each TMEM buffer before the MMAs that reuse it are issued
-  uint32_t g = 0, staged = 0;
+  // Iteration with s0 = k-blocks staged so far:
+  //   1. prefetch k-block s0 + 1 into registers
+  //   2. warp 0 issues the MMAs of k-block s0 - 1 (staged last iteration), so
+  //      the tensor pipe has work while k-block s0 is being staged
+  //   3. stage k-block s0 (3xTF32 split into smem); needs MMA s0 - STAGES done
+  //   4. fold the TMEM chunks ending at or before s0 - 2 (MMA s0 - 1 queued
+  //      behind them); once nothing is left to stage, fold everything
+  // A chunk's TMEM buffer is folded (step 4) an iteration before the MMAs
+  // that reuse it are issued (step 2), so no step waits on a later one.
+  uint32_t staged = 0;
   while (true) {
+    const uint32_t s0 = staged;
+    float2 nx[Cfg::kXPer], ny[Cfg::kYPer];
+    bool have_next = false;
     if (have) {
-      // 1. prefetch the next k-block into registers
-      float2 nx[Cfg::kXPer], ny[Cfg::kYPer];
-      const bool have_next = pc.u < units;
+      have_next = pc.u < units;
       if (have_next) {
         load(nx, ny);
         pc.next(p, units);
       }
-      // 2. split the current one into 3xTF32 planes of stage g % STAGES
-      const uint32_t s = staged % STAGES;
-      mbar_wait(&empty[s], ((staged / STAGES) & 1) ^ 1);
-      const uint32_t st = smem0 + s * Cfg::kStage;
-#pragma unroll
-      for (int i = 0; i < Cfg::kXPer; ++i) {
-        if (i < x_iters && x_act) {
-          const uint32_t a = st + (xs_lo ^ xhi_s[i]);
-          const float hr = tf32_rna(cx[i].x), hi = tf32_rna(cx[i].y);
-          sts2(a, hr, hi);
-          sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < Cfg::kYPer; ++i) {
-        if (i < y_iters && y_act) {
-          const uint32_t a0 = st + 2 * Cfg::kXPlane + (ys_lo ^ yhi_s[i]);
-          const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
-          const float hr = tf32_rna(cy[i].x), hi = tf32_rna(cy[i].y);
-          const float lr = cy[i].x - hr, li = cy[i].y - hi;
-          sts2(a0, hr, -hi);
-          sts2(a1, hi, hr);
-          sts2(a0 + Cfg::kYPlane, lr, -li);
-          sts2(a1 + Cfg::kYPlane, li, lr);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full[s]);
-      ++staged;
-#pragma unroll
-      for (int i = 0; i < Cfg::kXPer; ++i) cx[i] = nx[i];
-#pragma unroll
-      for (int i = 0; i < Cfg::kYPer; ++i) cy[i] = ny[i];
-      have = have_next;
     }
-    ++g;
-    // 3. warp 0 issues the MMAs of the staged k-blocks up to g-2
     if (warp == 0) {
-      while (ic.u < units && i_g + 1 < g && i_g < staged) {
+      while (i_g < s0) {
         if (i_in_chunk == 0) {
           const uint32_t b = i_ch & 1;
           mbar_wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
@@ -328,12 +302,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         for (int a = 0; a < Cfg::kAtoms; ++a) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t xo = st + a * Cfg::kXAtom + kk * 32;
-            const uint32_t yo = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
-            const uint64_t x_big = umma_desc_sw128(xo);
-            const uint64_t x_small = umma_desc_sw128(xo + Cfg::kXPlane);
-            const uint64_t y_big = umma_desc_sw128(yo);
-            const uint64_t y_small = umma_desc_sw128(yo + Cfg::kYPlane);
+            const uint32_t xs = st + a * Cfg::kXAtom + kk * 32;
+            const uint32_t ys = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
+            const uint64_t x_big = umma_desc_sw128(xs);
+            const uint64_t x_small = umma_desc_sw128(xs + Cfg::kXPlane);
+            const uint64_t y_big = umma_desc_sw128(ys);
+            const uint64_t y_small = umma_desc_sw128(ys + Cfg::kYPlane);
             const uint32_t acc0 = (i_in_chunk > 0 || a > 0 || kk > 0) ? 1u : 0u;
             // small products first: accumulated before the big one
             mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
@@ -352,13 +326,42 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         ic.next(p, units);
       }
     }
-    // 4. fold the chunks ending at or before g-3: their last MMAs were issued
-    //    an iteration ago and the following k-block's MMAs keep the tensor
-    //    pipe busy meanwhile
+    if (have) {
+      const uint32_t s = s0 % STAGES;
+      mbar_wait(&empty[s], ((s0 / STAGES) & 1) ^ 1);
+      const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) {
+        const uint32_t a = st + xadr(i);
+        const float hr = tf32_hi(cx[i].x), hi = tf32_hi(cx[i].y);
+        sts2(a, hr, hi);
+        sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) {
+        const uint32_t a0 = st + 2 * Cfg::kXPlane + yadr(i);
+        const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
+        const float hr = tf32_hi(cy[i].x), hi = tf32_hi(cy[i].y);
+        const float lr = cy[i].x - hr, li = cy[i].y - hi;
+        sts2(a0, hr, -hi);
+        sts2(a1, hi, hr);
+        sts2(a0 + Cfg::kYPlane, lr, -li);
+        sts2(a1 + Cfg::kYPlane, li, lr);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+      ++staged;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) cx[i] = nx[i];
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) cy[i] = ny[i];
+      have = have_next;
+    }
+    const bool drain = staged == s0;  // nothing staged: every MMA is issued
     while (fu < units) {
       const int64_t end = static_cast<int64_t>(f_c + 1) * p.chunk_kb;
       const int64_t last = static_cast<int64_t>(f_base) + (end < f_n ? end : f_n) - 1;
-      if (last + 3 > static_cast<int64_t>(g)) break;
+      if (!drain && last + 2 > static_cast<int64_t>(s0)) break;
       const uint32_t b = ch & 1;
       mbar_wait(&tfull[b], (ch >> 1) & 1);
       fence_after_sync();
@@ -397,13 +400,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
             for (int j = 0; j < Cfg::kHalf / 2; ++j)
               if (j < ncols) p.C[base + ocol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
           } else {
-            int64_t base = tab4(p.tabs + 2 * 1024, mb);
+            int64_t base = split * p.mn + tab4(p.tabs + 2 * 1024, mb);
             for (int j = 0; j < p.rbits; ++j)
               if ((r >> j) & 1) base += p.crow[j];
-            float2* dst = p.parts + split * p.mn + base + n0;
 #pragma unroll
             for (int j = 0; j < Cfg::kHalf / 2; ++j)
-              if (j < ncols) dst[j] = make_float2(acc[2 * j], acc[2 * j + 1]);
+              if (j < ncols) p.parts[base + ccol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
           }
         }
         f_base += static_cast<uint32_t>(f_n);
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         ++f_c;
       }
     }
-    if (!have && fu >= units) break;
+    if (drain && fu >= units) break;
   }
   fence_before_sync();
   __syncthreads();
@@ -467,6 +469,30 @@ uint32_t k_bit_addr(int j, uint32_t atom_bytes) {
   if (j <= 3) return 1u << (4 + j - 1);
   return (1u << (j - 4)) * atom_bytes;
 }
+// bank-selecting bits (byte address bits 3..6: the 8-byte slot in a 128-byte
+// wavefront of a half-warp's 8-byte stores)
+uint32_t bank4(uint32_t addr) { return (addr >> 3) & 15u; }
+
+// 2^(n - rank): ways of the worst bank conflict of n lane bits' address vectors
+int conflict_ways(const uint32_t* v, int n) {
+  uint32_t rows[8];
+  for (int i = 0; i < n; ++i) rows[i] = v[i];
+  int rank = 0;
+  for (int bit = 3; bit >= 0; --bit) {
+    int piv = -1;
+    for (int i = rank; i < n; ++i)
+      if ((rows[i] >> bit) & 1) {
+        piv = i;
+        break;
+      }
+    if (piv < 0) continue;
+    std::swap(rows[piv], rows[rank]);
+    for (int i = 0; i < n; ++i)
+      if (i != rank && ((rows[i] >> bit) & 1)) rows[i] ^= rows[rank];
+    ++rank;
+  }
+  return 1 << (n - rank);
+}
 
 double eff(int run) { return std::min(1.0, std::ldexp(1.0, run) / 4.0) + 0.1 * std::min(1.0, std::ldexp(1.0, run) / 16.0); }
 
@@ -485,12 +511,15 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   if (fy > 7) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: Y has more than 128 columns");
   if (fx < 6) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: X has fewer than 64 rows");
   const int nmma = std::max(32, 2 << fy);
+  const int lgn = nmma == 32 ? 4 : nmma == 64 ? 5 : nmma == 128 ? 6 : 7;  // log2(nmma / 2)
   const int kbc = nmma <= 64 ? 32 : 16;
   const int kb = kbc == 32 ? 5 : 4;
   if (c < kb) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: K smaller than one k-block");
   const int rb = std::min(7, fx);
   if (fx - rb > 32 || c - kb > 32) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: outer index > 32 bits");
 
+  // ---- which legs form the tile: greedy on the access efficiency of X
+  // reads, Y reads and output writes, weighted by their bytes
   const double rows_x = std::ldexp(1.0, fx), rows_y = std::ldexp(1.0, fy), kk = std::ldexp(1.0, c);
   const double wx = rows_x * kk, wy = rows_y * kk, wo = rows_x * rows_y;
   std::vector<int> xo(xf), yo(cm), oo(xf);  // per-tensor stride orders
@@ -515,8 +544,6 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
       if (!in(i)) return i;
     return -1;
   };
-  // greedy: each step adds the leg that most improves the access efficiency of
-  // X reads, Y reads or output writes (weighted by their bytes)
   while (nR < rb || nK < kb) {
     double best = 0;
     int pick = -1;
@@ -556,17 +583,138 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
       ++nK;
     }
   }
-  // bit assignments
-  std::vector<int> R, KL, outer_m, outer_k, ncols(yf);
-  for (int i : xf)
-    (inR[i] ? R : outer_m).push_back(i);
-  for (int i : cm)
-    (inK[i] ? KL : outer_k).push_back(i);
-  std::sort(R.begin(), R.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
-  std::sort(KL.begin(), KL.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::vector<int> R, KL, outer_m, outer_k;
+  for (int i : xf) (inR[i] ? R : outer_m).push_back(i);
+  for (int i : cm) (inK[i] ? KL : outer_k).push_back(i);
   std::sort(outer_m.begin(), outer_m.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
   std::sort(outer_k.begin(), outer_k.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
-  std::sort(ncols.begin(), ncols.end(), [&](int a, int b) { return legs[a].canon_stride < legs[b].canon_stride; });
+  // tile orders (real legs by stride; phantom bits, if any, come after)
+  std::vector<int> xt(R), yt(yf);
+  xt.insert(xt.end(), KL.begin(), KL.end());
+  yt.insert(yt.end(), KL.begin(), KL.end());
+  std::sort(xt.begin(), xt.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
+  std::sort(yt.begin(), yt.end(), [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
+
+  // ---- bit assignment: rows of R -> row bits, KL -> k bits, Y-free -> column
+  // bits.  A half-warp's 8-byte smem stores hit 16 distinct 8-byte slots iff
+  // the bank vectors of the operand's 4 fastest tile legs (thread bits 0-3)
+  // are independent; search the assignments that decide those vectors.
+  std::vector<int> row_of(n_legs, -1), k_of(n_legs, -1), n_of(n_legs, -1);
+  const int nxl = std::min<int>(4, static_cast<int>(xt.size())), nyl = std::min<int>(4, static_cast<int>(yt.size()));
+  auto vec_row = [](int j) { return j < 3 ? (1u << (1 + j)) : 0u; };
+  auto vec_k = [](int j) { return j == 0 ? 1u : (j <= 3 ? (1u << j) : 0u); };
+  auto vec_n = [](int j) { return j < 2 ? (1u << (2 + j)) : 0u; };
+  const double sx = 2.0 * 128 * kbc, sy = 4.0 * (nmma / 2) * kbc;  // smem store instructions
+  std::vector<int> lowR, lowN;  // low-order legs whose slots matter
+  for (int i = 0; i < nxl; ++i)
+    if (legs[xt[i]].kind == 0) lowR.push_back(xt[i]);
+  for (int i = 0; i < nyl; ++i)
+    if (legs[yt[i]].kind == 2) lowN.push_back(yt[i]);
+  std::vector<int> kperm(KL.size());
+  for (size_t i = 0; i < KL.size(); ++i) kperm[i] = static_cast<int>(i);
+  double best_score = 1e300;
+  std::vector<int> best_k, best_r, best_n;
+  // candidate slots: rows 0..min(rb,3)-1 or "high" (-1); columns 0..min(fy,2)-1 or high
+  auto enum_slots = [](int nlegs, int nslots, std::vector<std::vector<int>>& outv) {
+    std::vector<int> cur(nlegs, -1);
+    std::function<void(int, unsigned)> rec = [&](int i, unsigned used) {
+      if (i == nlegs) {
+        outv.push_back(cur);
+        return;
+      }
+      cur[i] = -1;
+      rec(i + 1, used);
+      for (int s = 0; s < nslots; ++s)
+        if (!((used >> s) & 1)) {
+          cur[i] = s;
+          rec(i + 1, used | (1u << s));
+        }
+    };
+    rec(0, 0);
+  };
+  std::vector<std::vector<int>> r_opts, n_opts;
+  enum_slots(static_cast<int>(lowR.size()), std::min(rb, 3), r_opts);
+  enum_slots(static_cast<int>(lowN.size()), std::min(fy, 2), n_opts);
+  do {
+    for (size_t i = 0; i < KL.size(); ++i) k_of[KL[kperm[i]]] = static_cast<int>(i);
+    double bx = 1e300, by = 1e300;
+    std::vector<int> br, bn;
+    for (auto& ro : r_opts) {
+      uint32_t v[4];
+      for (int i = 0; i < nxl; ++i) {
+        const int leg = xt[i];
+        if (legs[leg].kind == 1) {
+          v[i] = vec_k(k_of[leg]);
+        } else {
+          const int s = ro[std::find(lowR.begin(), lowR.end(), leg) - lowR.begin()];
+          v[i] = s < 0 ? 0u : vec_row(s);
+        }
+      }
+      const double sc = sx * conflict_ways(v, nxl);
+      if (sc < bx) {
+        bx = sc;
+        br = ro;
+      }
+    }
+    for (auto& no : n_opts) {
+      uint32_t v[4];
+      for (int i = 0; i < nyl; ++i) {
+        const int leg = yt[i];
+        if (legs[leg].kind == 1) {
+          v[i] = vec_k(k_of[leg]);
+        } else {
+          const int s = no[std::find(lowN.begin(), lowN.end(), leg) - lowN.begin()];
+          v[i] = s < 0 ? 0u : vec_n(s);
+        }
+      }
+      const double sc = sy * conflict_ways(v, nyl);
+      if (sc < by) {
+        by = sc;
+        bn = no;
+      }
+    }
+    if (bx + by < best_score) {
+      best_score = bx + by;
+      best_k.assign(KL.size(), 0);
+      for (size_t i = 0; i < KL.size(); ++i) best_k[i] = kperm[i];
+      best_r = br;
+      best_n = bn;
+    }
+  } while (std::next_permutation(kperm.begin(), kperm.end()));
+  for (size_t i = 0; i < KL.size(); ++i) k_of[KL[best_k[i]]] = static_cast<int>(i);
+  {  // rows: searched low legs first, the rest by output stride (lane-adjacent writes)
+    std::vector<char> used(7, 0);
+    for (size_t i = 0; i < lowR.size(); ++i)
+      if (best_r[i] >= 0) {
+        row_of[lowR[i]] = best_r[i];
+        used[best_r[i]] = 1;
+      }
+    std::vector<int> rest;
+    for (int leg : R)
+      if (row_of[leg] < 0) rest.push_back(leg);
+    std::sort(rest.begin(), rest.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
+    int slot = 0;
+    for (int leg : rest) {
+      while (used[slot]) ++slot;
+      row_of[leg] = slot;
+      used[slot] = 1;
+    }
+  }
+  {  // columns
+    std::vector<char> used(7, 0);
+    for (size_t i = 0; i < lowN.size(); ++i)
+      if (best_n[i] >= 0) {
+        n_of[lowN[i]] = best_n[i];
+        used[best_n[i]] = 1;
+      }
+    int slot = 0;
+    for (int leg : yf)
+      if (n_of[leg] < 0) {
+        while (used[slot]) ++slot;
+        n_of[leg] = slot;
+        used[slot] = 1;
+      }
+  }
 
   auto* plan = new GatherTcPlan();
   std::memset(&plan->p, 0, sizeof(plan->p));
@@ -579,36 +727,39 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   p.rbits = rb;
   p.fy = fy;
   const uint32_t xatom = 128 * 128, yatom = static_cast<uint32_t>(nmma) * 128;
-  auto pos = [](const std::vector<int>& v, int leg) {
-    return static_cast<int>(std::find(v.begin(), v.end(), leg) - v.begin());
-  };
-  {  // X tile bits by X stride
-    std::vector<int> bits(R);
-    bits.insert(bits.end(), KL.begin(), KL.end());
-    std::sort(bits.begin(), bits.end(), [&](int a, int b) { return legs[a].x_stride < legs[b].x_stride; });
-    p.nbx = static_cast<int>(bits.size());
-    for (int j = 0; j < p.nbx; ++j) {
-      const int leg = bits[j];
-      p.xg[j] = legs[leg].x_stride;
-      p.xs[j] = legs[leg].kind == 0 ? row_bit_addr(pos(R, leg)) : k_bit_addr(pos(KL, leg), xatom);
-    }
+  uint64_t xsum = 0, ysum = 0;
+  int j = 0;
+  for (int leg : xt) {
+    xsum += static_cast<uint64_t>(legs[leg].x_stride);
+    p.xg[j] = static_cast<uint32_t>(legs[leg].x_stride);
+    p.xs[j++] = legs[leg].kind == 0 ? row_bit_addr(row_of[leg]) : k_bit_addr(k_of[leg], xatom);
   }
-  {  // Y tile bits by Y stride; column n bit j <-> ncols[j], Y^ row 2n
-    std::vector<int> bits(ncols);
-    bits.insert(bits.end(), KL.begin(), KL.end());
-    std::sort(bits.begin(), bits.end(), [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
-    p.nby = static_cast<int>(bits.size());
-    for (int j = 0; j < p.nby; ++j) {
-      const int leg = bits[j];
-      p.yg[j] = legs[leg].y_stride;
-      p.ys[j] = legs[leg].kind == 2 ? row_bit_addr(pos(ncols, leg) + 1) : k_bit_addr(pos(KL, leg), yatom);
-    }
+  for (int r = rb; r < 7; ++r) {  // phantom rows: re-read rows, never stored
+    p.xg[j] = 0;
+    p.xs[j++] = row_bit_addr(r);
   }
-  for (int j = 0; j < rb; ++j) {
-    p.orow[j] = legs[R[j]].out_stride;
-    p.crow[j] = legs[R[j]].canon_stride;
+  j = 0;
+  for (int leg : yt) {
+    ysum += static_cast<uint64_t>(legs[leg].y_stride);
+    p.yg[j] = static_cast<uint32_t>(legs[leg].y_stride);
+    p.ys[j++] = legs[leg].kind == 2 ? row_bit_addr(n_of[leg] + 1) : k_bit_addr(k_of[leg], yatom);
   }
-  for (int j = 0; j < fy; ++j) p.ocol[j] = legs[ncols[j]].out_stride;
+  for (int n = fy; n < lgn; ++n) {  // phantom columns
+    p.yg[j] = 0;
+    p.ys[j++] = row_bit_addr(n + 1);
+  }
+  if (xsum >= (uint64_t{1} << 32) || ysum >= (uint64_t{1} << 32)) {
+    delete plan;
+    TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: tile offsets exceed 32 bits");
+  }
+  for (int leg : R) {
+    p.orow[row_of[leg]] = legs[leg].out_stride;
+    p.crow[row_of[leg]] = legs[leg].canon_stride;
+  }
+  for (int leg : yf) {
+    p.ocol[n_of[leg]] = legs[leg].out_stride;
+    p.ccol[n_of[leg]] = legs[leg].canon_stride;
+  }
   p.m_blocks = int64_t{1} << (fx - rb);
   p.kblocks = int64_t{1} << (c - kb);
   p.mn = plan->rows_x * plan->rows_y;
