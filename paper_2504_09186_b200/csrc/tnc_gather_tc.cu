@@ -51,9 +51,8 @@ using namespace tc5;
 constexpr int kGtWorkers = 256;
 constexpr int kGtWorkerWarps = kGtWorkers / 32;
 constexpr int kGtThreads = kGtWorkers;  // warp 0 also issues the MMAs
-constexpr int kGtMaxBits = 12;          // tile bits per operand (7 rows + 4 k; 6 cols + 4 k)
+constexpr int kGtMaxBits = 12;          // tile bits per operand (7 row/col + 5 k)
 constexpr int kGtTabs = 5;              // outer tables: xm, om, cm (m-block), xk, yk (k-block)
-constexpr int kGtKbc = 16;              // complex K per k-block: one 128-byte TF32 atom
 
 struct GtParams {
   const float2* X;
@@ -62,11 +61,9 @@ struct GtParams {
   float2* parts;        // [splits][rows_x * rows_y] canonical order (splits > 1)
   const int64_t* tabs;  // [kGtTabs][4][256] outer-index offset tables
   int64_t m_blocks, kblocks, mn;
-  int splits, chunk_kb, depth;
-  int nblocks;          // 1, or 2 when Y has 128 columns (one Y-free leg outside the tile)
-  int64_t y_nb, o_nb, c_nb;  // offsets of column block 1 in Y / the output / the partials
-  int rbits, fy;        // real row / column bits of the tile (phantom bits, stride 0, above)
-  // tile bit j (thread bit j for j < 8, element-slot bit j - 8 above): element
+  int splits, chunk_kb;
+  int rbits, fy;        // real row / column bits (phantom bits, stride 0, sit above)
+  // tile bit j (thread bit j for j < 8, iteration bit j - 8 above): element
   // offset in the operand and XOR-linear smem byte address in the stage plane
   uint32_t xg[kGtMaxBits], xs[kGtMaxBits];
   uint32_t yg[kGtMaxBits], ys[kGtMaxBits];
@@ -77,22 +74,26 @@ struct GtParams {
   int64_t dxk[32], dyk[32];
 };
 
-template <int NMMA, int STAGES>
+template <int NMMA, int KBC, int STAGES>
 struct GtCfg {
-  static constexpr int kLogN = NMMA == 32 ? 4 : NMMA == 64 ? 5 : 6;  // log2(NMMA / 2)
-  static constexpr int kXBits = 7 + 4;
-  static constexpr int kYBits = kLogN + 4;
+  static constexpr int kLogK = KBC == 32 ? 5 : 4;
+  static constexpr int kLogN = NMMA == 32 ? 4 : NMMA == 64 ? 5 : NMMA == 128 ? 6 : 7;  // log2(NMMA / 2)
+  static constexpr int kXBits = 7 + kLogK;
+  static constexpr int kYBits = kLogN + kLogK;
   static constexpr int kXPer = 1 << (kXBits - 8);  // X elements per thread per k-block
   static constexpr int kYPer = 1 << (kYBits - 8);
-  static constexpr int kXPlane = 128 * 128;         // one 128-row atom of TF32
-  static constexpr int kYPlane = NMMA * 128;
+  static constexpr bool kPre = NMMA <= 128;       // per-thread offsets kept in registers
+  static constexpr int kAtoms = KBC / 16;         // 128-byte (16 complex) K atoms per k-block
+  static constexpr int kXAtom = 128 * 128;
+  static constexpr int kYAtom = NMMA * 128;
+  static constexpr int kXPlane = kAtoms * kXAtom;
+  static constexpr int kYPlane = kAtoms * kYAtom;
   static constexpr int kStage = 2 * kXPlane + 2 * kYPlane;
   static constexpr int kSmem = STAGES * kStage + 1024;
   static constexpr int kHalf = NMMA / 2;
   static constexpr uint32_t kIdesc = idesc_f32acc(2, 128, NMMA);
   static_assert(kSmem + 4096 <= 227 * 1024, "smem budget");
-  static_assert(kYBits >= 8, "Y tile smaller than the CTA");
-  static_assert((NMMA / 2) * kGtKbc * 8 <= kXPlane, "raw Y tile must fit the X small plane");
+  static_assert(kXBits >= 8 && kYBits >= 8, "tile smaller than the CTA");
 };
 
 __device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
@@ -100,48 +101,22 @@ __device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
          __ldg(t + 512 + ((idx >> 16) & 255)) + __ldg(t + 768 + ((idx >> 24) & 255));
 }
 
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-
-// arrive on `bar` once every cp.async this thread issued so far has landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ float2 lds2(uint32_t a) {
+__device__ __forceinline__ float2 ldg_stream(const float2* p) {
   float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
+               : "l"(p));
   return v;
 }
 
-__device__ __forceinline__ float4 lds4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a)
-               : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
-  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
-}
-
-__device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, float d) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
-// TF32 "big" part, round-half-away on the 13 dropped mantissa bits
+// TF32 "big" part, round-half-away on the 13 dropped mantissa bits (two
+// integer ops; the tensor core reads only the top 19 bits of each fp32)
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-// x minus its TF32 truncation: the tensor core reads an fp32 operand as its
-// top 19 bits, so a raw fp32 plane is the "big" part and this is the "small"
-__device__ __forceinline__ float tf32_rem(float x) {
-  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+__device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }
 
 __device__ __forceinline__ void split_range(const GtParams& p, int split, int64_t& lo, int64_t& hi) {
@@ -154,27 +129,18 @@ __device__ __forceinline__ void split_range(const GtParams& p, int split, int64_
   }
 }
 
-// Unit / k-block cursor over this CTA's share of the (m-block, column block,
-// split) units; the unit's decomposition is computed once when it is opened
-// (32-bit divisions), never per k-block.
+// Unit / k-block cursor over this CTA's share of the (m-block, split) units;
+// the unit's decomposition is computed once when it is opened (32-bit
+// division), never per k-block.
 struct GtCursor {
-  uint32_t u, units;
-  uint32_t mb, split;
-  bool nb1;
+  uint32_t u, units, mb, split;
   int64_t kb, kb_hi;
   __device__ __forceinline__ bool valid() const { return u < units; }
   __device__ __forceinline__ void open(const GtParams& p) {
     if (u >= units) return;
     const uint32_t splits = static_cast<uint32_t>(p.splits);
-    const uint32_t rest = splits == 1 ? u : u / splits;
-    split = u - rest * splits;
-    if (p.nblocks == 1) {
-      mb = rest;
-      nb1 = false;
-    } else {
-      mb = rest >> 1;
-      nb1 = rest & 1;
-    }
+    mb = splits == 1 ? u : u / splits;
+    split = u - mb * splits;
     split_range(p, static_cast<int>(split), kb, kb_hi);
   }
   __device__ __forceinline__ void init(const GtParams& p, uint32_t n_units) {
@@ -191,24 +157,23 @@ struct GtCursor {
   }
 };
 
-template <int NMMA, int STAGES>
+template <int NMMA, int KBC, int STAGES>
 __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
-  using Cfg = GtCfg<NMMA, STAGES>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ uint64_t landed[STAGES], full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   __shared__ uint32_t xhi_g[16], xhi_s[16], yhi_g[16], yhi_s[16];
-  __shared__ int64_t ocol_t[64], ccol_t[64], dxk[32], dyk[32];
+  __shared__ int64_t ocol_t[128], ccol_t[128], dxk[32], dyk[32];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int t = threadIdx.x;
-  const uint32_t units = static_cast<uint32_t>(p.m_blocks * p.nblocks * p.splits);
+  const uint32_t units = static_cast<uint32_t>(p.m_blocks * p.splits);
 
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&landed[s], kGtWorkers);
       mbar_init(&full[s], kGtWorkers);
       mbar_init(&empty[s], 1);
     }
@@ -239,7 +204,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     dxk[t] = p.dxk[t];
     dyk[t] = p.dyk[t];
   }
-  if (t < 64) {
+  if (t < 128) {
     int64_t o = 0, c = 0;
     for (int j = 0; j < p.fy; ++j)
       if ((t >> j) & 1) {
@@ -273,60 +238,58 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       ys_lo ^= p.ys[j];
     }
   }
-  // this thread's tile elements: operand offsets and smem byte addresses
-  uint32_t xo[Cfg::kXPer], xa[Cfg::kXPer], yo[Cfg::kYPer], ya[Cfg::kYPer];
+  // per-thread element offsets / smem addresses of its tile elements
+  uint32_t xo[Cfg::kPre ? Cfg::kXPer : 1], xa[Cfg::kPre ? Cfg::kXPer : 1];
+  uint32_t yo[Cfg::kPre ? Cfg::kYPer : 1], ya[Cfg::kPre ? Cfg::kYPer : 1];
+  if constexpr (Cfg::kPre) {
 #pragma unroll
-  for (int i = 0; i < Cfg::kXPer; ++i) {
-    xo[i] = xg_lo + xhi_g[i];
-    xa[i] = xs_lo ^ xhi_s[i];
-  }
+    for (int i = 0; i < Cfg::kXPer; ++i) {
+      xo[i] = xg_lo + xhi_g[i];
+      xa[i] = xs_lo ^ xhi_s[i];
+    }
 #pragma unroll
-  for (int i = 0; i < Cfg::kYPer; ++i) {
-    yo[i] = yg_lo + yhi_g[i];
-    ya[i] = ys_lo ^ yhi_s[i];
+    for (int i = 0; i < Cfg::kYPer; ++i) {
+      yo[i] = yg_lo + yhi_g[i];
+      ya[i] = ys_lo ^ yhi_s[i];
+    }
   }
+  auto xoff = [&](int i) { if constexpr (Cfg::kPre) return xo[i]; else return xg_lo + xhi_g[i]; };
+  auto xadr = [&](int i) { if constexpr (Cfg::kPre) return xa[i]; else return xs_lo ^ xhi_s[i]; };
+  auto yoff = [&](int i) { if constexpr (Cfg::kPre) return yo[i]; else return yg_lo + yhi_g[i]; };
+  auto yadr = [&](int i) { if constexpr (Cfg::kPre) return ya[i]; else return ys_lo ^ yhi_s[i]; };
 
   float acc[Cfg::kHalf];
 #pragma unroll
   for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
 
-  GtCursor pc;  // loads (depth k-blocks ahead)
+  GtCursor pc;  // loads (one k-block ahead of the smem stores)
   pc.init(p, units);
-  // operand offsets of the load cursor's k-block: unit part + k-block part
-  int64_t xm_off = 0, xk_off = 0, yk_off = 0;
+  int64_t xm_off = 0, xk_off = 0, yk_off = 0;  // operand offsets of the load cursor's k-block
   auto open_offsets = [&]() {
     if (!pc.valid()) return;
     xm_off = tab4(p.tabs, pc.mb);
     xk_off = tab4(p.tabs + 3 * 1024, pc.kb);
-    yk_off = tab4(p.tabs + 4 * 1024, pc.kb) + (pc.nb1 ? p.y_nb : 0);
+    yk_off = tab4(p.tabs + 4 * 1024, pc.kb);
   };
   open_offsets();
   GtCursor ic;  // MMA issue (warp 0)
   ic.init(p, units);
   int i_in_chunk = 0;
-  uint32_t i_ch = 0;
+  uint32_t i_ch = 0, i_g = 0, dcol = 0;
   GtCursor fc;  // fold: this CTA's chunk sequence
   fc.init(p, units);
   int64_t f_n = fc.valid() ? fc.kb_hi - fc.kb : 0;
   int f_c = 0, f_nch = static_cast<int>((f_n + p.chunk_kb - 1) / p.chunk_kb);
   uint32_t f_base = 0, ch = 0;
 
-  // X tile: cp.async straight into the swizzled "big" plane of the stage.
-  // Raw Y tile: cp.async into the (still unused) "small" X plane, in a
-  // thread-linear layout; the conversion pass expands it into Y^.
-  uint32_t loaded = 0;
-  auto issue_loads = [&]() {
-    const uint32_t s = loaded % STAGES;
-    mbar_wait(&empty[s], ((loaded / STAGES) & 1) ^ 1);
-    const uint32_t st = smem0 + s * Cfg::kStage;
+  float2 cx[Cfg::kXPer], cy[Cfg::kYPer];
+  auto load = [&](float2 (&vx)[Cfg::kXPer], float2 (&vy)[Cfg::kYPer]) {
     const float2* xb = p.X + (xm_off + xk_off);
     const float2* yb = p.Y + yk_off;
 #pragma unroll
-    for (int i = 0; i < Cfg::kXPer; ++i) cp_async8(st + xa[i], xb + xo[i]);
+    for (int i = 0; i < Cfg::kXPer; ++i) vx[i] = ldg_stream(xb + xoff(i));
 #pragma unroll
-    for (int i = 0; i < Cfg::kYPer; ++i) cp_async8(st + Cfg::kXPlane + (i * kGtWorkers + t) * 8, yb + yo[i]);
-    cp_async_arrive(&landed[s]);
-    ++loaded;
+    for (int i = 0; i < Cfg::kYPer; ++i) vy[i] = __ldg(yb + yoff(i));
     const int b = __ffsll(pc.kb + 1) - 1;  // carry bit of kb -> kb + 1
     if (pc.next(p)) {
       open_offsets();
@@ -335,24 +298,102 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       yk_off += dyk[b];
     }
   };
-  for (int d = 0; d < p.depth && pc.valid(); ++d) issue_loads();
-
-  // Iteration j:
-  //   1. issue the loads of k-block j + depth (its stage is free once MMA
-  //      j + depth - STAGES is done: depth <= STAGES - 1)
-  //   2. fold the TMEM chunks ending at or before j - 2 (MMA j - 1 is queued
-  //      behind them); once k-blocks run out, fold everything
-  //   3. convert k-block j: Y raw -> Y^ big/small, X big -> X small
-  //   4. warp 0 issues the 12 MMAs of k-block j
-  // A chunk's TMEM buffer is folded (step 2) at least an iteration before the
-  // MMAs that reuse it are issued (step 4): no step waits on a later one.
-  for (uint32_t j = 0;; ++j) {
-    if (pc.valid()) issue_loads();
-    const bool more = j < loaded;
+  bool have = pc.valid();
+  if (have) load(cx, cy);
+  // Iteration with s0 = k-blocks staged so far:
+  //   1. prefetch k-block s0 + 1 into registers
+  //   2. warp 0 issues the MMAs of k-block s0 - 1 (staged last iteration), so
+  //      the tensor pipe has work while k-block s0 is being staged
+  //   3. stage k-block s0 (3xTF32 split into smem); needs MMA s0 - STAGES done
+  //   4. fold the TMEM chunks ending at or before s0 - 2 (MMA s0 - 1 queued
+  //      behind them); once nothing is left to stage, fold everything
+  // A chunk's TMEM buffer is folded (step 4) an iteration before the MMAs
+  // that reuse it are issued (step 2), so no step waits on a later one.
+  uint32_t staged = 0;
+  while (true) {
+    const uint32_t s0 = staged;
+    float2 nx[Cfg::kXPer], ny[Cfg::kYPer];
+    bool have_next = false;
+    if (have) {
+      have_next = pc.valid();
+      if (have_next) load(nx, ny);
+    }
+    if (warp == 0) {
+      while (i_g < s0) {
+        if (i_in_chunk == 0) {
+          const uint32_t b = i_ch & 1;
+          mbar_wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
+          fence_after_sync();
+          dcol = tmem_base + b * NMMA;
+        }
+        const uint32_t s = i_g % STAGES;
+        mbar_wait(&full[s], (i_g / STAGES) & 1);
+        fence_after_sync();
+        const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+        for (int a = 0; a < Cfg::kAtoms; ++a) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t xs = st + a * Cfg::kXAtom + kk * 32;
+            const uint32_t ys = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
+            const uint64_t x_big = umma_desc_sw128(xs);
+            const uint64_t x_small = umma_desc_sw128(xs + Cfg::kXPlane);
+            const uint64_t y_big = umma_desc_sw128(ys);
+            const uint64_t y_small = umma_desc_sw128(ys + Cfg::kYPlane);
+            const uint32_t acc0 = (i_in_chunk > 0 || a > 0 || kk > 0) ? 1u : 0u;
+            // small products first: accumulated before the big one
+            mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
+            mma_tf32_elect(dcol, x_big, y_small, Cfg::kIdesc, 1u);
+            mma_tf32_elect(dcol, x_big, y_big, Cfg::kIdesc, 1u);
+          }
+        }
+        mma_commit_elect(&empty[s]);
+        ++i_g;
+        const bool unit_end = ic.kb + 1 == ic.kb_hi;
+        if (++i_in_chunk == p.chunk_kb || unit_end) {
+          mma_commit_elect(&tfull[i_ch & 1]);
+          ++i_ch;
+          i_in_chunk = 0;
+        }
+        ic.next(p);
+      }
+    }
+    if (have) {
+      const uint32_t s = s0 % STAGES;
+      mbar_wait(&empty[s], ((s0 / STAGES) & 1) ^ 1);
+      const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) {
+        const uint32_t a = st + xadr(i);
+        const float hr = tf32_hi(cx[i].x), hi = tf32_hi(cx[i].y);
+        sts2(a, hr, hi);
+        sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) {
+        const uint32_t a0 = st + 2 * Cfg::kXPlane + yadr(i);
+        const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
+        const float hr = tf32_hi(cy[i].x), hi = tf32_hi(cy[i].y);
+        const float lr = cy[i].x - hr, li = cy[i].y - hi;
+        sts2(a0, hr, -hi);
+        sts2(a1, hi, hr);
+        sts2(a0 + Cfg::kYPlane, lr, -li);
+        sts2(a1 + Cfg::kYPlane, li, lr);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+      ++staged;
+#pragma unroll
+      for (int i = 0; i < Cfg::kXPer; ++i) cx[i] = nx[i];
+#pragma unroll
+      for (int i = 0; i < Cfg::kYPer; ++i) cy[i] = ny[i];
+      have = have_next;
+    }
+    const bool drain = staged == s0;  // nothing staged: every MMA is issued
     while (fc.valid()) {
       const int64_t end = static_cast<int64_t>(f_c + 1) * p.chunk_kb;
       const int64_t last = static_cast<int64_t>(f_base) + (end < f_n ? end : f_n) - 1;
-      if (more && last + 2 > static_cast<int64_t>(j)) break;
+      if (!drain && last + 2 > static_cast<int64_t>(s0)) break;
       const uint32_t b = ch & 1;
       mbar_wait(&tfull[b], (ch >> 1) & 1);
       fence_after_sync();
@@ -365,10 +406,10 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         tmem_wait_ld();
         if (f_c == 0) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) acc[gi * 16 + q] = __uint_as_float(v[q]);
+          for (int j = 0; j < 16; ++j) acc[gi * 16 + j] = __uint_as_float(v[j]);
         } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) acc[gi * 16 + q] += __uint_as_float(v[q]);
+          for (int j = 0; j < 16; ++j) acc[gi * 16 + j] += __uint_as_float(v[j]);
         }
       }
       fence_before_sync();
@@ -379,24 +420,23 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         // unit finished: store this thread's row (one TMEM lane), its column half
         const int r = quad * 32 + lane;
         const uint32_t mb = fc.mb, split = fc.split;
-        const bool nb1 = fc.nb1;
         if (r < (1 << p.rbits)) {
           const int n0 = half * (Cfg::kHalf / 2);
           const int ncols = min(Cfg::kHalf / 2, (1 << p.fy) - n0);
           if (p.splits == 1) {
-            int64_t base = tab4(p.tabs + 1 * 1024, mb) + (nb1 ? p.o_nb : 0);
-            for (int q = 0; q < p.rbits; ++q)
-              if ((r >> q) & 1) base += p.orow[q];
+            int64_t base = tab4(p.tabs + 1 * 1024, mb);
+            for (int j = 0; j < p.rbits; ++j)
+              if ((r >> j) & 1) base += p.orow[j];
 #pragma unroll
-            for (int q = 0; q < Cfg::kHalf / 2; ++q)
-              if (q < ncols) p.C[base + ocol_t[n0 + q]] = make_float2(acc[2 * q], acc[2 * q + 1]);
+            for (int j = 0; j < Cfg::kHalf / 2; ++j)
+              if (j < ncols) p.C[base + ocol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
           } else {
-            int64_t base = static_cast<int64_t>(split) * p.mn + tab4(p.tabs + 2 * 1024, mb) + (nb1 ? p.c_nb : 0);
-            for (int q = 0; q < p.rbits; ++q)
-              if ((r >> q) & 1) base += p.crow[q];
+            int64_t base = static_cast<int64_t>(split) * p.mn + tab4(p.tabs + 2 * 1024, mb);
+            for (int j = 0; j < p.rbits; ++j)
+              if ((r >> j) & 1) base += p.crow[j];
 #pragma unroll
-            for (int q = 0; q < Cfg::kHalf / 2; ++q)
-              if (q < ncols) p.parts[base + ccol_t[n0 + q]] = make_float2(acc[2 * q], acc[2 * q + 1]);
+            for (int j = 0; j < Cfg::kHalf / 2; ++j)
+              if (j < ncols) p.parts[base + ccol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
           }
         }
         f_base += static_cast<uint32_t>(f_n);
@@ -411,65 +451,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
         ++f_c;
       }
     }
-    if (!more) break;
-
-    const uint32_t s = j % STAGES;
-    const uint32_t st = smem0 + s * Cfg::kStage;
-    mbar_wait(&landed[s], (j / STAGES) & 1);
-#pragma unroll
-    for (int i = 0; i < Cfg::kYPer; ++i) {
-      const float2 y = lds2(st + Cfg::kXPlane + (i * kGtWorkers + t) * 8);
-      const uint32_t a0 = st + 2 * Cfg::kXPlane + ya[i];
-      const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
-      const float hr = tf32_hi(y.x), hi = tf32_hi(y.y);
-      const float lr = y.x - hr, li = y.y - hi;
-      sts2(a0, hr, -hi);
-      sts2(a1, hi, hr);
-      sts2(a0 + Cfg::kYPlane, lr, -li);
-      sts2(a1 + Cfg::kYPlane, li, lr);
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // raw Y read before X small overwrites it
-#pragma unroll
-    for (int c = 0; c < Cfg::kXPlane / (16 * kGtWorkers); ++c) {
-      const uint32_t a = st + (c * kGtWorkers + t) * 16;
-      const float4 v = lds4(a);
-      sts4(a + Cfg::kXPlane, tf32_rem(v.x), tf32_rem(v.y), tf32_rem(v.z), tf32_rem(v.w));
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(&full[s]);
-
-    if (warp == 0) {
-      if (i_in_chunk == 0) {
-        const uint32_t b = i_ch & 1;
-        mbar_wait_spin(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
-        fence_after_sync();
-      }
-      const uint32_t dcol = tmem_base + (i_ch & 1) * NMMA;
-      mbar_wait_spin(&full[s], (j / STAGES) & 1);
-      fence_after_sync();
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint32_t xs = st + kk * 32;
-        const uint32_t ys = st + 2 * Cfg::kXPlane + kk * 32;
-        const uint64_t x_big = umma_desc_sw128(xs);
-        const uint64_t x_small = umma_desc_sw128(xs + Cfg::kXPlane);
-        const uint64_t y_big = umma_desc_sw128(ys);
-        const uint64_t y_small = umma_desc_sw128(ys + Cfg::kYPlane);
-        const uint32_t acc0 = (i_in_chunk > 0 || kk > 0) ? 1u : 0u;
-        // small products first: accumulated before the big one
-        mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
-        mma_tf32_elect(dcol, x_big, y_small, Cfg::kIdesc, 1u);
-        mma_tf32_elect(dcol, x_big, y_big, Cfg::kIdesc, 1u);
-      }
-      mma_commit_elect(&empty[s]);
-      const bool unit_end = ic.kb + 1 == ic.kb_hi;
-      if (++i_in_chunk == p.chunk_kb || unit_end) {
-        mma_commit_elect(&tfull[i_ch & 1]);
-        ++i_ch;
-        i_in_chunk = 0;
-      }
-      ic.next(p);
-    }
+    if (drain && !fc.valid()) break;
   }
   fence_before_sync();
   __syncthreads();
@@ -483,7 +465,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 
 struct GatherTcPlan {
   GtParams p;
-  int nmma = 0, kbc = 0, stages = 0;
+  int nmma = 0, kbc = 0;
   int64_t rows_x = 0, rows_y = 0, k = 0;
   std::vector<int64_t> tabs_host;
   mutable std::mutex mu;
@@ -554,29 +536,21 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
     else if (legs[i].kind == 1) cm.push_back(i);
     else yf.push_back(i);
   }
-  const int fx = static_cast<int>(xf.size()), c = static_cast<int>(cm.size());
-  if (yf.size() > 7) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: Y has more than 128 columns");
+  const int fx = static_cast<int>(xf.size()), c = static_cast<int>(cm.size()),
+            fy = static_cast<int>(yf.size());
+  if (fy > 7) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: Y has more than 128 columns");
   if (fx < 6) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: X has fewer than 64 rows");
-  // 128 Y columns: the slowest Y-free leg selects one of two 64-column blocks
-  int nb_leg = -1;
-  if (yf.size() == 7) {
-    auto it = std::max_element(yf.begin(), yf.end(),
-                               [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
-    nb_leg = *it;
-    yf.erase(it);
-  }
-  const int fy = static_cast<int>(yf.size());
   const int nmma = std::max(32, 2 << fy);
-  const int lgn = nmma == 32 ? 4 : nmma == 64 ? 5 : 6;  // log2(nmma / 2)
-  const int kbc = kGtKbc;
-  const int kb = 4;
+  const int lgn = nmma == 32 ? 4 : nmma == 64 ? 5 : nmma == 128 ? 6 : 7;  // log2(nmma / 2)
+  const int kbc = nmma <= 64 ? 32 : 16;
+  const int kb = kbc == 32 ? 5 : 4;
   if (c < kb) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: K smaller than one k-block");
   const int rb = std::min(7, fx);
   if (fx - rb > 32 || c - kb > 32) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: outer index > 32 bits");
 
   // ---- which legs form the tile: greedy on the access efficiency of X
   // reads, Y reads and output writes, weighted by their bytes
-  const double rows_x = std::ldexp(1.0, fx), rows_y = std::ldexp(1.0, fy + (nb_leg >= 0)), kk = std::ldexp(1.0, c);
+  const double rows_x = std::ldexp(1.0, fx), rows_y = std::ldexp(1.0, fy), kk = std::ldexp(1.0, c);
   const double wx = rows_x * kk, wy = rows_y * kk, wo = rows_x * rows_y;
   std::vector<int> xo(xf), yo(cm), oo(xf);  // per-tensor stride orders
   xo.insert(xo.end(), cm.begin(), cm.end());
@@ -778,7 +752,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   plan->nmma = nmma;
   plan->kbc = kbc;
   plan->rows_x = int64_t{1} << fx;
-  plan->rows_y = int64_t{1} << (fy + (nb_leg >= 0));
+  plan->rows_y = int64_t{1} << fy;
   plan->k = int64_t{1} << c;
   p.rbits = rb;
   p.fy = fy;
@@ -817,12 +791,6 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
     p.ccol[n_of[leg]] = legs[leg].canon_stride;
   }
   p.m_blocks = int64_t{1} << (fx - rb);
-  p.nblocks = nb_leg >= 0 ? 2 : 1;
-  if (nb_leg >= 0) {
-    p.y_nb = legs[nb_leg].y_stride;
-    p.o_nb = legs[nb_leg].out_stride;
-    p.c_nb = legs[nb_leg].canon_stride;
-  }
   p.kblocks = int64_t{1} << (c - kb);
   p.mn = plan->rows_x * plan->rows_y;
   // outer tables
@@ -854,11 +822,11 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   // k-splits: enough units for every SM, each SM's share within ~3% of the others
   const int sms = num_sms();
   int splits = 1;
-  if (p.m_blocks * p.nblocks < 4 * sms) {
+  if (p.m_blocks < 4 * sms) {
     double best_eff = 0;
     const int64_t smax = std::min<int64_t>(p.kblocks, 4096);
     for (int64_t s = 1; s <= smax; ++s) {
-      const int64_t units = p.m_blocks * p.nblocks * s;
+      const int64_t units = p.m_blocks * s;
       const double e = static_cast<double>(units) / (ceil_div(units, sms) * sms);
       if (e > best_eff + 1e-9) {
         best_eff = e;
@@ -874,13 +842,6 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   p.splits = splits;
   p.chunk_kb = std::max(1, 32 / kbc);
   if (const char* env = std::getenv("TNC_GT_CHUNK")) p.chunk_kb = std::max(1, std::atoi(env));
-  // loads in flight: every free stage for narrow tiles (short MMAs); one
-  // stage kept back for 64-column tiles so a load never waits on the MMA
-  // just issued
-  plan->stages = nmma == 32 ? 5 : nmma == 64 ? 4 : 3;
-  p.depth = plan->stages - 2;
-  if (const char* env = std::getenv("TNC_GT_DEPTH"))
-    p.depth = std::max(1, std::min(plan->stages - 1, std::atoi(env)));
   *out = plan;
   return TNC_OK;
 }
@@ -891,10 +852,10 @@ void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
 
 namespace {
 
-template <int NMMA, int STAGES>
+template <int NMMA, int KBC, int STAGES>
 int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
-  using Cfg = GtCfg<NMMA, STAGES>;
-  auto kern = gather_tc_kernel<NMMA, STAGES>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
   ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
@@ -923,14 +884,15 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
   p.tabs = plan->tabs_dev;
   if (p.splits == 1 && !p.C) TNC_RET(TNC_ERR_INVALID, "tc_gather: null output");
   if (p.splits > 1 && !p.parts) TNC_RET(TNC_ERR_INVALID, "tc_gather: null partials");
-  const int64_t units = p.m_blocks * p.nblocks * p.splits;
+  const int64_t units = p.m_blocks * p.splits;
   const double M = static_cast<double>(plan->rows_x), N = static_cast<double>(plan->rows_y),
                K = static_cast<double>(plan->k);
   const double flops = 8.0 * M * N * K, bytes = 8.0 * (M * K + N * K + M * N);
   switch (plan->nmma) {
-    case 32: return launch_gt<32, 5>(p, units, flops, bytes, stream);
-    case 64: return launch_gt<64, 4>(p, units, flops, bytes, stream);
-    case 128: return launch_gt<128, 3>(p, units, flops, bytes, stream);
+    case 32: return launch_gt<32, 32, 2>(p, units, flops, bytes, stream);
+    case 64: return launch_gt<64, 32, 2>(p, units, flops, bytes, stream);
+    case 128: return launch_gt<128, 16, 3>(p, units, flops, bytes, stream);
+    case 256: return launch_gt<256, 16, 2>(p, units, flops, bytes, stream);
     default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
   }
 }
