@@ -272,6 +272,11 @@ bool build_gather_splitk(tnc_plan* p) {
   return true;
 }
 
+int env_flag(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 // 3xFP16 (2x-rate kind::f16, half the operand bytes) unless TNC_TC_TF32=1
 int default_tc_variant() {
   const char* v = std::getenv("TNC_TC_TF32");
@@ -607,7 +612,23 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
       return st;
     }
   }
-  if (want == TNC_VARIANT_TCGATHER) {
+  // K6 (operands gathered in-kernel, tensor cores) takes over the CUDA-core
+  // split-K, the streaming kernel and the tensor-core steps that are narrow
+  // (<= 64 Y columns: the permute + split passes over X cost more than the
+  // GEMM) or split-K shaped (one row of 128-row tiles per SM at most)
+  // whenever the step fits its envelope.  TNC_TCGATHER=0 disables it.
+  if (variant == TNC_VARIANT_AUTO && p->dtype == TNC_C64 && env_flag("TNC_TCGATHER", 1) &&
+      (want == TNC_VARIANT_SPLITK || want == TNC_VARIANT_STREAM ||
+       (tc && (p->rows_y <= 64 || p->rows_x <= 128 * static_cast<int64_t>(num_sms())))) &&
+      p->rows_x >= 64 && p->rows_y <= 128 && k >= 16) {
+    if (try_gather_tc(p, free_a, free_b) == TNC_OK) {
+      if (p->stream) {
+        stream_destroy(p->stream);
+        p->stream = nullptr;
+      }
+      want = TNC_VARIANT_TCGATHER;
+    }
+  } else if (want == TNC_VARIANT_TCGATHER) {
     const int st = try_gather_tc(p, free_a, free_b);
     if (st != TNC_OK) {
       delete p;

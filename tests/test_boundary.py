@@ -2,6 +2,7 @@
 mapping, and the oracle quarantine.  CPU only (no kernel launches)."""
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
@@ -74,10 +75,18 @@ def test_plan_shapes_and_output_order_host_only():
     # tiny output, huge K -> the CUDA-core split-K reduction is auto-selected
     code, info, _ = _plan([("m", 2)] + [(f"k{i}", 2) for i in range(14)], [(f"k{i}", 2) for i in range(14)] + [("n", 4)])
     assert code == 0 and info.variant == 3
-    # narrow step (C1a-like): the K5 streaming kernel, no workspace at all
-    code, info, _ = _plan([(f"a{i}", 2) for i in range(16)] + [(f"k{i}", 2) for i in range(6)],
-                          [(f"k{i}", 2) for i in range(6)] + [(f"b{i}", 2) for i in range(4)],
-                          out=[f"b{i}" for i in range(4)] + [f"a{i}" for i in range(16)])
+    # narrow step (C1a-like): the K6 gather-fed tensor-core kernel ...
+    narrow = ([(f"a{i}", 2) for i in range(16)] + [(f"k{i}", 2) for i in range(6)],
+              [(f"k{i}", 2) for i in range(6)] + [(f"b{i}", 2) for i in range(4)])
+    out = [f"b{i}" for i in range(4)] + [f"a{i}" for i in range(16)]
+    code, info, _ = _plan(*narrow, out=out)
+    assert code == 0 and info.variant == 6
+    # ... or, with K6 switched off, the K5 streaming kernel (no workspace at all)
+    os.environ["TNC_TCGATHER"] = "0"
+    try:
+        code, info, _ = _plan(*narrow, out=out)
+    finally:
+        del os.environ["TNC_TCGATHER"]
     assert code == 0 and info.variant == 5 and info.workspace_bytes == 0
 
 
