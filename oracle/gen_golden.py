@@ -8,7 +8,7 @@ travel instead.
 
     python oracle/gen_golden.py [section ...]
 
-Sections: perm contract split c0 plans sliced reuse pairs
+Sections: perm contract split c0 plans sliced reuse pairs spill
 """
 
 from __future__ import annotations
@@ -375,9 +375,39 @@ def section_pairs():
     _dump("pairs", {"cases": out})
 
 
+def section_spill():
+    """Reference byte formats: the TNCPART1 partials spill of the 4x4 sliced
+    run (execute.py:473-490) and DenseTensor.to_bytes (tensor.py:146-161)."""
+    import tempfile
+
+    from tncsim.execute import write_partials
+
+    wl = workloads.CircuitWorkload(4, 4, 10, 3, 3)
+    circ = tncsim.parse_circuit(workloads.grid_circuit_text(wl.rows, wl.cols, wl.cycles, wl.seed))
+    closed = tncsim.circuit_to_network(circ, "0" * circ.n_qubits)
+    t = tncsim.greedy_path(closed, 0)
+    spec = tncsim.select_slices(t, 7, 64, 0)
+    res = tncsim.run_sliced(closed, t, spec, "single")
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "p.bin")
+        write_partials(path, res)
+        raw = open(path, "rb").read()
+    rng = np.random.default_rng(5)
+    tens = []
+    for prec, dt in (("single", np.complex64), ("double", np.complex128)):
+        data = rand_c(rng, 12, dt)
+        tt = tncsim.DenseTensor([RIndex("ab", 3), RIndex("c", 4)], data, precision=prec)
+        tens.append({"precision": prec, "labels": ["ab", "c"], "dims": [3, 4], "data": _c(data),
+                     "bytes": base64.b64encode(tt.to_bytes()).decode()})
+    _dump("spill", {"labels": list(res.partial_labels), "dims": list(res.partial_dims),
+                    "partials": [[list(k), _f(v)] for k, v in sorted(res.partials.items())],
+                    "spill_b64": base64.b64encode(raw).decode(), "tensors": tens})
+
+
 SECTIONS = {
     "perm": section_perm, "contract": section_contract, "split": section_split, "c0": section_c0,
     "plans": section_plans, "sliced": section_sliced, "reuse": section_reuse, "pairs": section_pairs,
+    "spill": section_spill,
 }
 
 if __name__ == "__main__":

@@ -62,7 +62,8 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the executor imports torch.distributed lazily; keep `import` cheap
     if name in {"ReductionTopology", "RunResult", "RunStats", "hierarchical_reduce", "run_direct",
-                "run_reuse", "run_reuse_open", "run_sliced", "run_open", "SliceExecutor"}:
+                "run_reuse", "run_reuse_open", "run_sliced", "run_open", "SliceExecutor", "read_partials",
+                "write_partials"}:
         from . import execute
 
         return getattr(execute, name)

@@ -25,6 +25,8 @@ with fp64 arithmetic (CUDA cores).
 from __future__ import annotations
 
 import itertools
+import json
+import struct
 import time
 from dataclasses import dataclass
 from typing import Callable, Iterable, Sequence
@@ -79,6 +81,53 @@ class RunResult:
     partials: dict
     partial_labels: tuple[str, ...]
     partial_dims: tuple[int, ...]
+
+
+# -- partial-result spill files (reference execute.py:468-506) ----------------
+
+SPILL_MAGIC = b"TNCPART1"
+
+
+def write_partials(path: str, result: RunResult) -> None:
+    """Binary spill of a run's per-slice partials, byte-compatible with the
+    reference (``execute.py:473-490``): magic, u32 header length, JSON header
+    ``{"labels", "dims"}``, u64 count, then ``(u64 code, f64 re, f64 im)``
+    records in sorted key order, ``code = code * dim + value`` (first label most
+    significant, ``execute.py:481-484``)."""
+    head = json.dumps({"labels": list(result.partial_labels), "dims": list(result.partial_dims)}).encode()
+    with open(path, "wb") as fh:
+        fh.write(SPILL_MAGIC)
+        fh.write(struct.pack("<I", len(head)))
+        fh.write(head)
+        fh.write(struct.pack("<Q", len(result.partials)))
+        for key in sorted(result.partials):
+            code = 0
+            for v, d in zip(key, result.partial_dims):
+                code = code * d + v
+            val = complex(result.partials[key])
+            fh.write(struct.pack("<Qdd", code, val.real, val.imag))
+
+
+def read_partials(path: str) -> tuple[tuple[str, ...], tuple[int, ...], dict]:
+    """Inverse of :func:`write_partials` (reference ``execute.py:493-506``);
+    raises ``TncError`` on a foreign file."""
+    with open(path, "rb") as fh:
+        if fh.read(len(SPILL_MAGIC)) != SPILL_MAGIC:
+            raise TncError(f"{path}: not a partials spill file")
+        (hlen,) = struct.unpack("<I", fh.read(4))
+        head = json.loads(fh.read(hlen).decode())
+        labels = tuple(head["labels"])
+        dims = tuple(head["dims"])
+        (count,) = struct.unpack("<Q", fh.read(8))
+        partials = {}
+        for _ in range(count):
+            code, re, im = struct.unpack("<Qdd", fh.read(24))
+            key = []
+            for d in reversed(dims):
+                key.append(code % d)
+                code //= d
+            partials[tuple(reversed(key))] = complex(re, im)
+    return labels, dims, partials
 
 
 def hierarchical_reduce(partials: Sequence, topo: ReductionTopology):
