@@ -20,8 +20,9 @@
 // K = 2^15 contraction accumulated in TMEM alone would miss the 1e-5 contract.
 // The MMA warp therefore accumulates short K-chunks (kb_per_chunk k-blocks)
 // into alternating TMEM buffers and the epilogue warps fold each finished
-// chunk into fp32 registers with round-to-nearest adds (chain-length error
-// ~4e-7 per GEMM independent of K).
+// chunk into fp32 registers with round-to-nearest adds (error independent of
+// K: ~4e-7 per GEMM with 32-complex-K chunks, ~1e-6 with the 128-K chunks
+// the 3xFP16 path uses by default).
 //
 // Roles (320 threads, persistent over (split, m, n) work units):
 //   warp 0     TMA producer (one elected lane)
@@ -769,8 +770,10 @@ int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, cons
   // raster group of 64 m-blocks: measured best on the C3/C4 GEMM shapes (+2-4% over 16;
   // >= 128 loses ~15%), ncu DRAM reads 818 -> 579 GB on the 2^(15,15,14) step
   p.group_m = std::max(1, env_int("TNC_GROUP_M", 64));
-  // chunk = 32 complex K per TMEM accumulation chain (see header comment)
-  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", 64 / Cfg::kBK));
+  // TMEM accumulation chain per register fold (see header comment): 128
+  // complex K for 3xFP16 (measured rel-L2 ~1e-6 per GEMM; 32 K gives ~4e-7
+  // but folds 4x as often, -2.5 % on C3 under the power cap), 32 for 3xTF32
+  p.kb_per_chunk = std::max(1, env_int("TNC_CHUNK_KB", (F16 ? 256 : 64) / Cfg::kBK));
   p.C = static_cast<float2*>(C);
   p.ldcm = ldcm;
   p.ldcn = ldcn;
