@@ -20,7 +20,7 @@
 //   unit     = (m-block, k-split); persistent CTAs stride over units
 //   complex  = one real GEMM: X interleaved [M, 2K] times the expanded Y^
 //              (rows 2n = (Yr, -Yi), 2n+1 = (Yi, Yr)) gives interleaved C
-//   accuracy = chunks of 32 complex K accumulate in alternating TMEM buffers
+//   accuracy = chunks of 128 complex K accumulate in alternating TMEM buffers
 //              and are folded into fp32 registers (same scheme as K2)
 //   output   = one split: C written in its FINAL (caller's) leg order; more
 //              splits: fp32 partials [split][row][col] (canonical order),
@@ -840,7 +840,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
     if (forced >= 1) splits = static_cast<int>(std::min<int64_t>(forced, p.kblocks));
   }
   p.splits = splits;
-  p.chunk_kb = std::max(1, 32 / kbc);
+  p.chunk_kb = std::max(1, 128 / kbc);  // 128 complex K per TMEM chain (as K2)
   if (const char* env = std::getenv("TNC_GT_CHUNK")) p.chunk_kb = std::max(1, std::atoi(env));
   *out = plan;
   return TNC_OK;
