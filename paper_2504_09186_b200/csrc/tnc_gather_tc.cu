@@ -72,6 +72,8 @@ struct GtParams {
   // outer k-block index kb -> kb + 1 flips bit b = ctz(kb + 1) on and the bits
   // below it off: X / Y offsets move by these carry deltas
   int64_t dxk[32], dyk[32];
+  // same for the m-block index mb -> mb + 1: X, final-output, partial offsets
+  int64_t dxm[32], dom[32], dcm[32];
 };
 
 template <int NMMA, int KBC, int STAGES>
@@ -119,41 +121,51 @@ __device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }
 
-__device__ __forceinline__ void split_range(const GtParams& p, int split, int64_t& lo, int64_t& hi) {
+__device__ __forceinline__ void split_range(const GtParams& p, int split, uint32_t& lo, uint32_t& hi) {
   if (p.splits == 1) {
     lo = 0;
-    hi = p.kblocks;
+    hi = static_cast<uint32_t>(p.kblocks);
   } else {
-    lo = p.kblocks * split / p.splits;
-    hi = p.kblocks * (split + 1) / p.splits;
+    lo = static_cast<uint32_t>(p.kblocks * split / p.splits);
+    hi = static_cast<uint32_t>(p.kblocks * (split + 1) / p.splits);
   }
 }
 
-// Unit / k-block cursor over this CTA's share of the (m-block, split) units;
-// the unit's decomposition is computed once when it is opened (32-bit
-// division), never per k-block.
+// Unit / k-block cursor over this CTA's contiguous range of (m-block,
+// split) units (split fastest).  Consecutive units move mb by at most one,
+// so owners advance their m-block offsets with carry deltas instead of table
+// lookups; the only division happens once, at init.
 struct GtCursor {
-  uint32_t u, units, mb, split;
-  int64_t kb, kb_hi;
-  __device__ __forceinline__ bool valid() const { return u < units; }
-  __device__ __forceinline__ void open(const GtParams& p) {
-    if (u >= units) return;
+  uint32_t u, u_end, mb, split;
+  int carry;  // after next() == 2: the bit of mb that turned on
+  uint32_t kb, kb_hi;
+  __device__ __forceinline__ bool valid() const { return u < u_end; }
+  __device__ __forceinline__ void init(const GtParams& p, uint32_t units) {
+    u = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * units / gridDim.x);
+    u_end = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x + 1) * units / gridDim.x);
     const uint32_t splits = static_cast<uint32_t>(p.splits);
     mb = splits == 1 ? u : u / splits;
     split = u - mb * splits;
+    carry = 0;
     split_range(p, static_cast<int>(split), kb, kb_hi);
   }
-  __device__ __forceinline__ void init(const GtParams& p, uint32_t n_units) {
-    u = blockIdx.x;
-    units = n_units;
-    open(p);
+  // advance one unit: 1 = same m-block (next split), 2 = next m-block
+  __device__ __forceinline__ int next_unit(const GtParams& p) {
+    ++u;
+    int moved = 1;
+    if (++split == static_cast<uint32_t>(p.splits)) {
+      split = 0;
+      ++mb;
+      carry = __ffs(mb) - 1;
+      moved = 2;
+    }
+    if (valid()) split_range(p, static_cast<int>(split), kb, kb_hi);
+    return moved;
   }
-  // advance one k-block; true when the cursor entered a new unit
-  __device__ __forceinline__ bool next(const GtParams& p) {
-    if (++kb < kb_hi) return false;
-    u += gridDim.x;
-    open(p);
-    return true;
+  // advance one k-block: 0 = same unit, else next_unit()'s code
+  __device__ __forceinline__ int next(const GtParams& p) {
+    if (++kb < kb_hi) return 0;
+    return next_unit(p);
   }
 };
 
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   __shared__ uint32_t xhi_g[16], xhi_s[16], yhi_g[16], yhi_s[16];
-  __shared__ int64_t ocol_t[128], ccol_t[128], dxk[32], dyk[32];
+  __shared__ int64_t ocol_t[128], ccol_t[128], dxk[32], dyk[32], dxm[32], dom[32], dcm[32];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   const int warp = threadIdx.x >> 5;
@@ -203,6 +215,9 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   if (t < 32) {
     dxk[t] = p.dxk[t];
     dyk[t] = p.dyk[t];
+    dxm[t] = p.dxm[t];
+    dom[t] = p.dom[t];
+    dcm[t] = p.dcm[t];
   }
   if (t < 128) {
     int64_t o = 0, c = 0;
@@ -264,20 +279,23 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 
   GtCursor pc;  // loads (one k-block ahead of the smem stores)
   pc.init(p, units);
-  int64_t xm_off = 0, xk_off = 0, yk_off = 0;  // operand offsets of the load cursor's k-block
-  auto open_offsets = [&]() {
+  // operand offsets of the load cursor's k-block
+  int64_t xm_off = pc.valid() ? tab4(p.tabs, pc.mb) : 0, xk_off = 0, yk_off = 0;
+  auto open_k = [&]() {  // first k-block of the cursor's (new) unit
     if (!pc.valid()) return;
-    xm_off = tab4(p.tabs, pc.mb);
-    xk_off = tab4(p.tabs + 3 * 1024, pc.kb);
-    yk_off = tab4(p.tabs + 4 * 1024, pc.kb);
+    xk_off = pc.kb == 0 ? 0 : tab4(p.tabs + 3 * 1024, pc.kb);
+    yk_off = pc.kb == 0 ? 0 : tab4(p.tabs + 4 * 1024, pc.kb);
   };
-  open_offsets();
+  open_k();
   GtCursor ic;  // MMA issue (warp 0)
   ic.init(p, units);
   int i_in_chunk = 0;
   uint32_t i_ch = 0, i_g = 0, dcol = 0;
   GtCursor fc;  // fold: this CTA's chunk sequence
   fc.init(p, units);
+  // final-output (one split) or partial-layout offset of the fold cursor's m-block
+  const int64_t* dmo = p.splits == 1 ? dom : dcm;
+  int64_t m_off = fc.valid() ? tab4(p.tabs + (p.splits == 1 ? 1 : 2) * 1024, fc.mb) : 0;
   int64_t f_n = fc.valid() ? fc.kb_hi - fc.kb : 0;
   int f_c = 0, f_nch = static_cast<int>((f_n + p.chunk_kb - 1) / p.chunk_kb);
   uint32_t f_base = 0, ch = 0;
@@ -290,12 +308,14 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     for (int i = 0; i < Cfg::kXPer; ++i) vx[i] = ldg_stream(xb + xoff(i));
 #pragma unroll
     for (int i = 0; i < Cfg::kYPer; ++i) vy[i] = __ldg(yb + yoff(i));
-    const int b = __ffsll(pc.kb + 1) - 1;  // carry bit of kb -> kb + 1
-    if (pc.next(p)) {
-      open_offsets();
-    } else {
+    const int b = __ffs(pc.kb + 1) - 1;  // carry bit of kb -> kb + 1
+    const int moved = pc.next(p);
+    if (moved == 0) {
       xk_off += dxk[b];
       yk_off += dyk[b];
+    } else {
+      if (moved == 2) xm_off += dxm[pc.carry];
+      open_k();
     }
   };
   bool have = pc.valid();
@@ -419,19 +439,19 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       if (f_c == f_nch - 1) {
         // unit finished: store this thread's row (one TMEM lane), its column half
         const int r = quad * 32 + lane;
-        const uint32_t mb = fc.mb, split = fc.split;
+        const uint32_t split = fc.split;
         if (r < (1 << p.rbits)) {
           const int n0 = half * (Cfg::kHalf / 2);
           const int ncols = min(Cfg::kHalf / 2, (1 << p.fy) - n0);
           if (p.splits == 1) {
-            int64_t base = tab4(p.tabs + 1 * 1024, mb);
+            int64_t base = m_off;
             for (int j = 0; j < p.rbits; ++j)
               if ((r >> j) & 1) base += p.orow[j];
 #pragma unroll
             for (int j = 0; j < Cfg::kHalf / 2; ++j)
               if (j < ncols) p.C[base + ocol_t[n0 + j]] = make_float2(acc[2 * j], acc[2 * j + 1]);
           } else {
-            int64_t base = static_cast<int64_t>(split) * p.mn + tab4(p.tabs + 2 * 1024, mb);
+            int64_t base = static_cast<int64_t>(split) * p.mn + m_off;
             for (int j = 0; j < p.rbits; ++j)
               if ((r >> j) & 1) base += p.crow[j];
 #pragma unroll
@@ -440,8 +460,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
           }
         }
         f_base += static_cast<uint32_t>(f_n);
-        fc.u += gridDim.x;
-        fc.open(p);
+        if (fc.next_unit(p) == 2) m_off += dmo[fc.carry];
         f_c = 0;
         if (fc.valid()) {
           f_n = fc.kb_hi - fc.kb;
@@ -546,7 +565,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   const int kb = kbc == 32 ? 5 : 4;
   if (c < kb) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: K smaller than one k-block");
   const int rb = std::min(7, fx);
-  if (fx - rb > 32 || c - kb > 32) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: outer index > 32 bits");
+  if (fx - rb > 31 || c - kb > 31) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: outer index > 31 bits");
 
   // ---- which legs form the tile: greedy on the access efficiency of X
   // reads, Y reads and output writes, weighted by their bytes
@@ -810,15 +829,19 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   build_tab4(scm, plan->tabs_host.data() + 2 * 1024);
   build_tab4(sxk, plan->tabs_host.data() + 3 * 1024);
   build_tab4(syk, plan->tabs_host.data() + 4 * 1024);
-  for (int b = 0; b < 32; ++b) {
-    int64_t dx = 0, dy = 0;
-    for (int i = 0; i <= b && i < static_cast<int>(sxk.size()); ++i) {
-      dx += i == b ? sxk[i] : -sxk[i];
-      dy += i == b ? syk[i] : -syk[i];
+  // carry deltas: index i -> i + 1 turns bit b = ctz(i + 1) on, bits < b off
+  auto carry_deltas = [](const std::vector<int64_t>& st, int64_t* out) {
+    for (int b = 0; b < 32; ++b) {
+      int64_t d = 0;
+      for (int i = 0; i <= b && i < static_cast<int>(st.size()); ++i) d += i == b ? st[i] : -st[i];
+      out[b] = d;
     }
-    p.dxk[b] = dx;
-    p.dyk[b] = dy;
-  }
+  };
+  carry_deltas(sxk, p.dxk);
+  carry_deltas(syk, p.dyk);
+  carry_deltas(sxm, p.dxm);
+  carry_deltas(som, p.dom);
+  carry_deltas(scm, p.dcm);
   // k-splits: enough units for every SM, each SM's share within ~3% of the others
   const int sms = num_sms();
   int splits = 1;
