@@ -153,10 +153,17 @@ def make_desc(labels_ids, dims, strides, dtype) -> TensorDesc:
 
 
 def stream_ptr(stream=None) -> int:
+    """Raw cudaStream_t of ``stream`` (default: torch's current stream on the
+    current device).  The per-step launch path calls this for every
+    contraction, so the default case avoids building a Stream object."""
     import torch
 
-    s = torch.cuda.current_stream() if stream is None else stream
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(torch.cuda.current_device()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def env_flag(name: str, default: str = "") -> str:

@@ -137,9 +137,10 @@ def contract_into(plan: ContractPlan, a_data: torch.Tensor, b_data: torch.Tensor
     if out is None:
         out = torch.empty(dims, dtype=a_data.dtype, device=a_data.device)
     ws_n = plan.workspace_bytes
-    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=a_data.device)
+    ws = torch.empty(ws_n, dtype=torch.uint8, device=a_data.device) if ws_n else None
     _lib.check(_lib.load().tnc_contract(plan.handle, a_data.data_ptr(), b_data.data_ptr(),
-                                        out.data_ptr(), ws.data_ptr(), ws_n, _lib.stream_ptr()))
+                                        out.data_ptr(), ws.data_ptr() if ws is not None else None, ws_n,
+                                        _lib.stream_ptr()))
     return out
 
 

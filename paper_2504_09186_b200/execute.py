@@ -152,6 +152,28 @@ def _slice_keys(dims: Sequence[int]) -> Iterable[tuple[int, ...]]:
     return itertools.product(*[range(d) for d in dims])
 
 
+def _leaves_at(tensors: Sequence[DenseTensor], precision: str) -> list[DenseTensor]:
+    """Leaves at storage precision on the device (reference ``execute.py:128``
+    rounds them to the run precision).  Leaves that need a copy are converted
+    in one batched device pass (one concatenate, one cast) and handed out as
+    views: a circuit network has hundreds of tiny leaves, and per-leaf casts
+    made the host side of an end-to-end call launch-bound."""
+    out: list[DenseTensor | None] = list(tensors)
+    todo = [i for i, t in enumerate(tensors) if not (t.precision == precision and t.data.is_cuda)]
+    if not todo:
+        return list(tensors)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    flat = torch.cat([tensors[i].data.reshape(-1).to(dev, non_blocking=True) for i in todo])
+    flat = flat.to(DTYPES[precision])
+    pos = 0
+    for i in todo:
+        t = tensors[i]
+        n = t.size
+        out[i] = DenseTensor.__new__(DenseTensor)._init_raw(t.indices, flat[pos:pos + n].view(t.dims))
+        pos += n
+    return out
+
+
 class Engine:
     """Per-run device state: leaves at storage precision, counters."""
 
@@ -162,8 +184,7 @@ class Engine:
         self.precision = precision
         self.rate = ELEMENT_BYTES[precision]
         self.cap = max_intermediate_bytes
-        self.leaves = [t if t.precision == precision and t.data.is_cuda else t.astype(precision)
-                       for t in net.tensors]
+        self.leaves = _leaves_at(net.tensors, precision)
 
     def fetch(self, s: LinearSchedule, ref: int, assignment: dict[str, int], values: dict) -> DenseTensor:
         if ref < s.n_leaves:
@@ -521,8 +542,21 @@ class SliceExecutor:
             st = self.s.steps[p]
             needed.update((st.lhs, st.rhs))
         values: dict = {}
-        for p in self.invariant_positions:
-            self.eng.run_range(self.s, p + 1, p + 1, {}, values, self.stats)
+        eng, s = self.eng, self.s
+        if eng.cap is not None:  # the reference step loop enforces the cap per step
+            for p in self.invariant_positions:
+                eng.run_range(s, p + 1, p + 1, {}, values, self.stats)
+        else:
+            # lean loop: hundreds of tiny steps, so no per-step accounting
+            # (SSA values are consumed exactly once; the totals are exact)
+            for p in self.invariant_positions:
+                st = s.steps[p]
+                out = eng.contract(eng.fetch(s, st.lhs, {}, values), eng.fetch(s, st.rhs, {}, values))
+                for ref in (st.lhs, st.rhs):
+                    if ref >= s.n_leaves:
+                        values.pop(ref, None)
+                values[st.result] = out
+            self.stats.multiplies += self.multiplies_invariant
         self.cache = {k: v for k, v in values.items() if k in needed or k == self.root}
         self._prepared = True
 
