@@ -103,6 +103,26 @@ __device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
          __ldg(t + 512 + ((idx >> 16) & 255)) + __ldg(t + 768 + ((idx >> 24) & 255));
 }
 
+// Element-slot part (tile bits >= the thread bits) of an offset / address:
+// thread-independent, so with i unrolled the sums come straight from the
+// parameter bank on the uniform datapath (no shared-memory round trip).
+template <int FIRST, int LAST>
+__device__ __forceinline__ uint32_t slot_sum(const uint32_t (&tab)[kGtMaxBits], int i) {
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = FIRST; j < LAST; ++j)
+    if ((i >> (j - FIRST)) & 1) s += tab[j];
+  return s;
+}
+template <int FIRST, int LAST>
+__device__ __forceinline__ uint32_t slot_xor(const uint32_t (&tab)[kGtMaxBits], int i) {
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = FIRST; j < LAST; ++j)
+    if ((i >> (j - FIRST)) & 1) s ^= tab[j];
+  return s;
+}
+
 __device__ __forceinline__ float2 ldg_stream(const float2* p) {
   float2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
@@ -175,7 +195,6 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
-  __shared__ uint32_t xhi_g[16], xhi_s[16], yhi_g[16], yhi_s[16];
   __shared__ int64_t ocol_t[128], ccol_t[128], dxk[32], dyk[32], dxm[32], dom[32], dcm[32];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -194,23 +213,6 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       mbar_init(&tempty[b], kGtWorkerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (t < 16) {
-    uint32_t g = 0, s = 0, h = 0, q = 0;
-    for (int j = 8; j < Cfg::kXBits; ++j)
-      if ((t >> (j - 8)) & 1) {
-        g += p.xg[j];
-        s ^= p.xs[j];
-      }
-    for (int j = 8; j < Cfg::kYBits; ++j)
-      if ((t >> (j - 8)) & 1) {
-        h += p.yg[j];
-        q ^= p.ys[j];
-      }
-    xhi_g[t] = g;
-    xhi_s[t] = s;
-    yhi_g[t] = h;
-    yhi_s[t] = q;
   }
   if (t < 32) {
     dxk[t] = p.dxk[t];
@@ -259,19 +261,31 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   if constexpr (Cfg::kPre) {
 #pragma unroll
     for (int i = 0; i < Cfg::kXPer; ++i) {
-      xo[i] = xg_lo + xhi_g[i];
-      xa[i] = xs_lo ^ xhi_s[i];
+      xo[i] = xg_lo + slot_sum<8, Cfg::kXBits>(p.xg, i);
+      xa[i] = xs_lo ^ slot_xor<8, Cfg::kXBits>(p.xs, i);
     }
 #pragma unroll
     for (int i = 0; i < Cfg::kYPer; ++i) {
-      yo[i] = yg_lo + yhi_g[i];
-      ya[i] = ys_lo ^ yhi_s[i];
+      yo[i] = yg_lo + slot_sum<8, Cfg::kYBits>(p.yg, i);
+      ya[i] = ys_lo ^ slot_xor<8, Cfg::kYBits>(p.ys, i);
     }
   }
-  auto xoff = [&](int i) { if constexpr (Cfg::kPre) return xo[i]; else return xg_lo + xhi_g[i]; };
-  auto xadr = [&](int i) { if constexpr (Cfg::kPre) return xa[i]; else return xs_lo ^ xhi_s[i]; };
-  auto yoff = [&](int i) { if constexpr (Cfg::kPre) return yo[i]; else return yg_lo + yhi_g[i]; };
-  auto yadr = [&](int i) { if constexpr (Cfg::kPre) return ya[i]; else return ys_lo ^ yhi_s[i]; };
+  auto xoff = [&](int i) {
+    if constexpr (Cfg::kPre) return xo[i];
+    else return xg_lo + slot_sum<8, Cfg::kXBits>(p.xg, i);
+  };
+  auto xadr = [&](int i) {
+    if constexpr (Cfg::kPre) return xa[i];
+    else return xs_lo ^ slot_xor<8, Cfg::kXBits>(p.xs, i);
+  };
+  auto yoff = [&](int i) {
+    if constexpr (Cfg::kPre) return yo[i];
+    else return yg_lo + slot_sum<8, Cfg::kYBits>(p.yg, i);
+  };
+  auto yadr = [&](int i) {
+    if constexpr (Cfg::kPre) return ya[i];
+    else return ys_lo ^ slot_xor<8, Cfg::kYBits>(p.ys, i);
+  };
 
   float acc[Cfg::kHalf];
 #pragma unroll
