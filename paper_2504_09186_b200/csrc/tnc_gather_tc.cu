@@ -26,6 +26,11 @@
 //              splits: fp32 partials [split][row][col] (canonical order),
 //              then the fixed-order tree reduction
 //
+// Paired layout: when X's stride-1 leg is a common tile leg it sits on k bit
+// 0, so (k, k + 1) pairs are 16 contiguous bytes in HBM and in the swizzled
+// plane: one 16-byte load and one 16-byte store per plane move two elements
+// (Y likewise when the same leg is Y's stride-1 leg).
+//
 // Roles (256 threads, 8 warps = 2 per SM sub-partition so each thread can
 // hold up to 255 registers): every warp gathers + splits (loads run one
 // k-block ahead of the smem stores), folds TMEM lane quadrant w % 4, column
@@ -36,6 +41,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "tnc_common.cuh"
@@ -76,14 +82,17 @@ struct GtParams {
   int64_t dxm[32], dom[32], dcm[32];
 };
 
-template <int NMMA, int KBC, int STAGES>
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
 struct GtCfg {
   static constexpr int kLogK = KBC == 32 ? 5 : 4;
   static constexpr int kLogN = NMMA == 32 ? 4 : NMMA == 64 ? 5 : NMMA == 128 ? 6 : 7;  // log2(NMMA / 2)
-  static constexpr int kXBits = 7 + kLogK;
-  static constexpr int kYBits = kLogN + kLogK;
-  static constexpr int kXPer = 1 << (kXBits - 8);  // X elements per thread per k-block
+  // tile bits of the gathered element grid (a paired leg is inside the element)
+  static constexpr int kXBits = 7 + kLogK - (PX ? 1 : 0);
+  static constexpr int kYBits = kLogN + kLogK - (PY ? 1 : 0);
+  static constexpr int kXPer = 1 << (kXBits - 8);  // X elements (or pairs) per thread per k-block
   static constexpr int kYPer = 1 << (kYBits - 8);
+  using XT = typename std::conditional<PX, float4, float2>::type;
+  using YT = typename std::conditional<PY, float4, float2>::type;
   static constexpr bool kPre = NMMA <= 128;       // per-thread offsets kept in registers
   static constexpr int kAtoms = KBC / 16;         // 128-byte (16 complex) K atoms per k-block
   static constexpr int kXAtom = 128 * 128;
@@ -135,6 +144,19 @@ __device__ __forceinline__ float2 ldg_stream(const float2* p) {
 // integer ops; the tensor core reads only the top 19 bits of each fp32)
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ float4 ldg_stream4(const float2* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
 }
 
 __device__ __forceinline__ void sts2(uint32_t addr, float a, float b) {
@@ -189,9 +211,9 @@ struct GtCursor {
   }
 };
 
-template <int NMMA, int KBC, int STAGES>
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
 __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
-  using Cfg = GtCfg<NMMA, KBC, STAGES>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
@@ -314,14 +336,23 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   int f_c = 0, f_nch = static_cast<int>((f_n + p.chunk_kb - 1) / p.chunk_kb);
   uint32_t f_base = 0, ch = 0;
 
-  float2 cx[Cfg::kXPer], cy[Cfg::kYPer];
-  auto load = [&](float2 (&vx)[Cfg::kXPer], float2 (&vy)[Cfg::kYPer]) {
+  using XT = typename Cfg::XT;
+  using YT = typename Cfg::YT;
+  XT cx[Cfg::kXPer];
+  YT cy[Cfg::kYPer];
+  auto load = [&](XT (&vx)[Cfg::kXPer], YT (&vy)[Cfg::kYPer]) {
     const float2* xb = p.X + (xm_off + xk_off);
     const float2* yb = p.Y + yk_off;
 #pragma unroll
-    for (int i = 0; i < Cfg::kXPer; ++i) vx[i] = ldg_stream(xb + xoff(i));
+    for (int i = 0; i < Cfg::kXPer; ++i) {
+      if constexpr (PX) vx[i] = ldg_stream4(xb + xoff(i));
+      else vx[i] = ldg_stream(xb + xoff(i));
+    }
 #pragma unroll
-    for (int i = 0; i < Cfg::kYPer; ++i) vy[i] = __ldg(yb + yoff(i));
+    for (int i = 0; i < Cfg::kYPer; ++i) {
+      if constexpr (PY) vy[i] = __ldg(reinterpret_cast<const float4*>(yb + yoff(i)));
+      else vy[i] = __ldg(yb + yoff(i));
+    }
     const int b = __ffs(pc.kb + 1) - 1;  // carry bit of kb -> kb + 1
     const int moved = pc.next(p);
     if (moved == 0) {
@@ -346,7 +377,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   uint32_t staged = 0;
   while (true) {
     const uint32_t s0 = staged;
-    float2 nx[Cfg::kXPer], ny[Cfg::kYPer];
+    XT nx[Cfg::kXPer];
+    YT ny[Cfg::kYPer];
     bool have_next = false;
     if (have) {
       have_next = pc.valid();
@@ -399,20 +431,35 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 #pragma unroll
       for (int i = 0; i < Cfg::kXPer; ++i) {
         const uint32_t a = st + xadr(i);
-        const float hr = tf32_hi(cx[i].x), hi = tf32_hi(cx[i].y);
-        sts2(a, hr, hi);
-        sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+        if constexpr (PX) {  // (k, k + 1) pair: 16 contiguous bytes per plane
+          const float r0 = tf32_hi(cx[i].x), i0 = tf32_hi(cx[i].y), r1 = tf32_hi(cx[i].z), i1 = tf32_hi(cx[i].w);
+          sts4(a, r0, i0, r1, i1);
+          sts4(a + Cfg::kXPlane, cx[i].x - r0, cx[i].y - i0, cx[i].z - r1, cx[i].w - i1);
+        } else {
+          const float hr = tf32_hi(cx[i].x), hi = tf32_hi(cx[i].y);
+          sts2(a, hr, hi);
+          sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+        }
       }
 #pragma unroll
       for (int i = 0; i < Cfg::kYPer; ++i) {
         const uint32_t a0 = st + 2 * Cfg::kXPlane + yadr(i);
         const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
-        const float hr = tf32_hi(cy[i].x), hi = tf32_hi(cy[i].y);
-        const float lr = cy[i].x - hr, li = cy[i].y - hi;
-        sts2(a0, hr, -hi);
-        sts2(a1, hi, hr);
-        sts2(a0 + Cfg::kYPlane, lr, -li);
-        sts2(a1 + Cfg::kYPlane, li, lr);
+        if constexpr (PY) {
+          const float r0 = tf32_hi(cy[i].x), i0 = tf32_hi(cy[i].y), r1 = tf32_hi(cy[i].z), i1 = tf32_hi(cy[i].w);
+          const float lr0 = cy[i].x - r0, li0 = cy[i].y - i0, lr1 = cy[i].z - r1, li1 = cy[i].w - i1;
+          sts4(a0, r0, -i0, r1, -i1);
+          sts4(a1, i0, r0, i1, r1);
+          sts4(a0 + Cfg::kYPlane, lr0, -li0, lr1, -li1);
+          sts4(a1 + Cfg::kYPlane, li0, lr0, li1, lr1);
+        } else {
+          const float hr = tf32_hi(cy[i].x), hi = tf32_hi(cy[i].y);
+          const float lr = cy[i].x - hr, li = cy[i].y - hi;
+          sts2(a0, hr, -hi);
+          sts2(a1, hi, hr);
+          sts2(a0 + Cfg::kYPlane, lr, -li);
+          sts2(a1 + Cfg::kYPlane, li, lr);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&full[s]);
@@ -498,6 +545,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 
 struct GatherTcPlan {
   GtParams p;
+  GtParams p2;              // paired layout (16-byte K pairs), when pair_x
+  bool pair_x = false, pair_y = false;
   int nmma = 0, kbc = 0;
   int64_t rows_x = 0, rows_y = 0, k = 0;
   std::vector<int64_t> tabs_host;
@@ -662,122 +711,171 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   // bits.  A half-warp's 8-byte smem stores hit 16 distinct 8-byte slots iff
   // the bank vectors of the operand's 4 fastest tile legs (thread bits 0-3)
   // are independent; search the assignments that decide those vectors.
-  std::vector<int> row_of(n_legs, -1), k_of(n_legs, -1), n_of(n_legs, -1);
-  const int nxl = std::min<int>(4, static_cast<int>(xt.size())), nyl = std::min<int>(4, static_cast<int>(yt.size()));
-  auto vec_row = [](int j) { return j < 3 ? (1u << (1 + j)) : 0u; };
-  auto vec_k = [](int j) { return j == 0 ? 1u : (j <= 3 ? (1u << j) : 0u); };
-  auto vec_n = [](int j) { return j < 2 ? (1u << (2 + j)) : 0u; };
-  const double sx = 2.0 * 128 * kbc, sy = 4.0 * (nmma / 2) * kbc;  // smem store instructions
-  std::vector<int> lowR, lowN;  // low-order legs whose slots matter
-  for (int i = 0; i < nxl; ++i)
-    if (legs[xt[i]].kind == 0) lowR.push_back(xt[i]);
-  for (int i = 0; i < nyl; ++i)
-    if (legs[yt[i]].kind == 2) lowN.push_back(yt[i]);
-  std::vector<int> kperm(KL.size());
-  for (size_t i = 0; i < KL.size(); ++i) kperm[i] = static_cast<int>(i);
-  double best_score = 1e300;
-  std::vector<int> best_k, best_r, best_n;
-  // candidate slots: rows 0..min(rb,3)-1 or "high" (-1); columns 0..min(fy,2)-1 or high
-  auto enum_slots = [](int nlegs, int nslots, std::vector<std::vector<int>>& outv) {
-    std::vector<int> cur(nlegs, -1);
-    std::function<void(int, unsigned)> rec = [&](int i, unsigned used) {
-      if (i == nlegs) {
-        outv.push_back(cur);
-        return;
-      }
-      cur[i] = -1;
-      rec(i + 1, used);
-      for (int s = 0; s < nslots; ++s)
-        if (!((used >> s) & 1)) {
-          cur[i] = s;
-          rec(i + 1, used | (1u << s));
-        }
+  // Paired mode (px / py): the operand's stride-1 leg is a common leg placed on
+  // k bit 0, so each thread moves K-adjacent element pairs as 16 bytes (one
+  // global load, one store per plane); then a quarter-warp's 16-byte stores
+  // must hit 8 distinct 16-byte chunks (vectors over address bits 4-6 of the
+  // next 3 legs).
+  const uint32_t xatom = 128 * 128, yatom = static_cast<uint32_t>(nmma) * 128;
+  auto assign = [&](bool px, bool py, GtParams& q) -> int {
+    std::vector<int> row_of(n_legs, -1), k_of(n_legs, -1), n_of(n_legs, -1);
+    std::vector<int> xl(xt.begin() + (px ? 1 : 0), xt.end()), yl(yt.begin() + (py ? 1 : 0), yt.end());
+    const int xlanes = px ? 3 : 4, ylanes = py ? 3 : 4;
+    const int nxl = std::min<int>(xlanes, static_cast<int>(xl.size()));
+    const int nyl = std::min<int>(ylanes, static_cast<int>(yl.size()));
+    auto vec_row = [&](int j, bool chunk) { return chunk ? (j < 3 ? 1u << j : 0u) : (j < 3 ? (1u << (1 + j)) : 0u); };
+    auto vec_k = [&](int j, bool chunk) {
+      if (chunk) return (j >= 1 && j <= 3) ? 1u << (j - 1) : 0u;
+      return j == 0 ? 1u : (j <= 3 ? (1u << j) : 0u);
     };
-    rec(0, 0);
-  };
-  std::vector<std::vector<int>> r_opts, n_opts;
-  enum_slots(static_cast<int>(lowR.size()), std::min(rb, 3), r_opts);
-  enum_slots(static_cast<int>(lowN.size()), std::min(fy, 2), n_opts);
-  do {
-    for (size_t i = 0; i < KL.size(); ++i) k_of[KL[kperm[i]]] = static_cast<int>(i);
-    double bx = 1e300, by = 1e300;
-    std::vector<int> br, bn;
-    for (auto& ro : r_opts) {
-      uint32_t v[4];
-      for (int i = 0; i < nxl; ++i) {
-        const int leg = xt[i];
-        if (legs[leg].kind == 1) {
-          v[i] = vec_k(k_of[leg]);
-        } else {
-          const int s = ro[std::find(lowR.begin(), lowR.end(), leg) - lowR.begin()];
-          v[i] = s < 0 ? 0u : vec_row(s);
+    auto vec_n = [&](int j, bool chunk) { return chunk ? (j < 2 ? 1u << (j + 1) : 0u) : (j < 2 ? (1u << (2 + j)) : 0u); };
+    // smem store instructions per k-block
+    const double sx = (px ? 1.0 : 2.0) * 128 * kbc, sy = (py ? 2.0 : 4.0) * (nmma / 2) * kbc;
+    std::vector<int> lowR, lowN;  // low-order legs whose slots matter
+    for (int i = 0; i < nxl; ++i)
+      if (legs[xl[i]].kind == 0) lowR.push_back(xl[i]);
+    for (int i = 0; i < nyl; ++i)
+      if (legs[yl[i]].kind == 2) lowN.push_back(yl[i]);
+    std::vector<int> kperm(KL.size());
+    for (size_t i = 0; i < KL.size(); ++i) kperm[i] = static_cast<int>(i);
+    double best_score = 1e300;
+    std::vector<int> best_k, best_r, best_n;
+    // candidate slots: rows 0..min(rb,3)-1 or "high" (-1); columns 0..min(fy,2)-1 or high
+    auto enum_slots = [](int nlegs, int nslots, std::vector<std::vector<int>>& outv) {
+      std::vector<int> cur(nlegs, -1);
+      std::function<void(int, unsigned)> rec = [&](int i, unsigned used) {
+        if (i == nlegs) {
+          outv.push_back(cur);
+          return;
+        }
+        cur[i] = -1;
+        rec(i + 1, used);
+        for (int s = 0; s < nslots; ++s)
+          if (!((used >> s) & 1)) {
+            cur[i] = s;
+            rec(i + 1, used | (1u << s));
+          }
+      };
+      rec(0, 0);
+    };
+    std::vector<std::vector<int>> r_opts, n_opts;
+    enum_slots(static_cast<int>(lowR.size()), std::min(rb, 3), r_opts);
+    enum_slots(static_cast<int>(lowN.size()), std::min(fy, 2), n_opts);
+    do {
+      for (size_t i = 0; i < KL.size(); ++i) k_of[KL[kperm[i]]] = static_cast<int>(i);
+      if (px && k_of[xt[0]] != 0) continue;  // the paired leg must sit on k bit 0
+      double bx = 1e300, by = 1e300;
+      std::vector<int> br, bn;
+      for (auto& ro : r_opts) {
+        uint32_t v[4];
+        for (int i = 0; i < nxl; ++i) {
+          const int leg = xl[i];
+          if (legs[leg].kind == 1) {
+            v[i] = vec_k(k_of[leg], px);
+          } else {
+            const int sl = ro[std::find(lowR.begin(), lowR.end(), leg) - lowR.begin()];
+            v[i] = sl < 0 ? 0u : vec_row(sl, px);
+          }
+        }
+        const double sc = sx * conflict_ways(v, nxl);
+        if (sc < bx) {
+          bx = sc;
+          br = ro;
         }
       }
-      const double sc = sx * conflict_ways(v, nxl);
-      if (sc < bx) {
-        bx = sc;
-        br = ro;
-      }
-    }
-    for (auto& no : n_opts) {
-      uint32_t v[4];
-      for (int i = 0; i < nyl; ++i) {
-        const int leg = yt[i];
-        if (legs[leg].kind == 1) {
-          v[i] = vec_k(k_of[leg]);
-        } else {
-          const int s = no[std::find(lowN.begin(), lowN.end(), leg) - lowN.begin()];
-          v[i] = s < 0 ? 0u : vec_n(s);
+      for (auto& no : n_opts) {
+        uint32_t v[4];
+        for (int i = 0; i < nyl; ++i) {
+          const int leg = yl[i];
+          if (legs[leg].kind == 1) {
+            v[i] = vec_k(k_of[leg], py);
+          } else {
+            const int sl = no[std::find(lowN.begin(), lowN.end(), leg) - lowN.begin()];
+            v[i] = sl < 0 ? 0u : vec_n(sl, py);
+          }
+        }
+        const double sc = sy * conflict_ways(v, nyl);
+        if (sc < by) {
+          by = sc;
+          bn = no;
         }
       }
-      const double sc = sy * conflict_ways(v, nyl);
-      if (sc < by) {
-        by = sc;
-        bn = no;
+      if (bx + by < best_score) {
+        best_score = bx + by;
+        best_k.assign(KL.size(), 0);
+        for (size_t i = 0; i < KL.size(); ++i) best_k[i] = kperm[i];
+        best_r = br;
+        best_n = bn;
       }
-    }
-    if (bx + by < best_score) {
-      best_score = bx + by;
-      best_k.assign(KL.size(), 0);
-      for (size_t i = 0; i < KL.size(); ++i) best_k[i] = kperm[i];
-      best_r = br;
-      best_n = bn;
-    }
-  } while (std::next_permutation(kperm.begin(), kperm.end()));
-  for (size_t i = 0; i < KL.size(); ++i) k_of[KL[best_k[i]]] = static_cast<int>(i);
-  {  // rows: searched low legs first, the rest by output stride (lane-adjacent writes)
-    std::vector<char> used(7, 0);
-    for (size_t i = 0; i < lowR.size(); ++i)
-      if (best_r[i] >= 0) {
-        row_of[lowR[i]] = best_r[i];
-        used[best_r[i]] = 1;
-      }
-    std::vector<int> rest;
-    for (int leg : R)
-      if (row_of[leg] < 0) rest.push_back(leg);
-    std::sort(rest.begin(), rest.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
-    int slot = 0;
-    for (int leg : rest) {
-      while (used[slot]) ++slot;
-      row_of[leg] = slot;
-      used[slot] = 1;
-    }
-  }
-  {  // columns
-    std::vector<char> used(7, 0);
-    for (size_t i = 0; i < lowN.size(); ++i)
-      if (best_n[i] >= 0) {
-        n_of[lowN[i]] = best_n[i];
-        used[best_n[i]] = 1;
-      }
-    int slot = 0;
-    for (int leg : yf)
-      if (n_of[leg] < 0) {
+    } while (std::next_permutation(kperm.begin(), kperm.end()));
+    for (size_t i = 0; i < KL.size(); ++i) k_of[KL[best_k[i]]] = static_cast<int>(i);
+    {  // rows: searched low legs first, the rest by output stride (lane-adjacent writes)
+      std::vector<char> used(7, 0);
+      for (size_t i = 0; i < lowR.size(); ++i)
+        if (best_r[i] >= 0) {
+          row_of[lowR[i]] = best_r[i];
+          used[best_r[i]] = 1;
+        }
+      std::vector<int> rest;
+      for (int leg : R)
+        if (row_of[leg] < 0) rest.push_back(leg);
+      std::sort(rest.begin(), rest.end(), [&](int a, int b) { return legs[a].out_stride < legs[b].out_stride; });
+      int slot = 0;
+      for (int leg : rest) {
         while (used[slot]) ++slot;
-        n_of[leg] = slot;
+        row_of[leg] = slot;
         used[slot] = 1;
       }
-  }
+    }
+    {  // columns
+      std::vector<char> used(7, 0);
+      for (size_t i = 0; i < lowN.size(); ++i)
+        if (best_n[i] >= 0) {
+          n_of[lowN[i]] = best_n[i];
+          used[best_n[i]] = 1;
+        }
+      int slot = 0;
+      for (int leg : yf)
+        if (n_of[leg] < 0) {
+          while (used[slot]) ++slot;
+          n_of[leg] = slot;
+          used[slot] = 1;
+        }
+    }
+    // tile bit tables (a paired leg is the 16-byte element, not a bit)
+    uint64_t xsum = 0, ysum = 0;
+    int j = 0;
+    for (int leg : xl) {
+      xsum += static_cast<uint64_t>(legs[leg].x_stride);
+      q.xg[j] = static_cast<uint32_t>(legs[leg].x_stride);
+      q.xs[j++] = legs[leg].kind == 0 ? row_bit_addr(row_of[leg]) : k_bit_addr(k_of[leg], xatom);
+    }
+    for (int r = rb; r < 7; ++r) {  // phantom rows: re-read rows, never stored
+      q.xg[j] = 0;
+      q.xs[j++] = row_bit_addr(r);
+    }
+    j = 0;
+    for (int leg : yl) {
+      ysum += static_cast<uint64_t>(legs[leg].y_stride);
+      q.yg[j] = static_cast<uint32_t>(legs[leg].y_stride);
+      q.ys[j++] = legs[leg].kind == 2 ? row_bit_addr(n_of[leg] + 1) : k_bit_addr(k_of[leg], yatom);
+    }
+    for (int n = fy; n < lgn; ++n) {  // phantom columns
+      q.yg[j] = 0;
+      q.ys[j++] = row_bit_addr(n + 1);
+    }
+    if (xsum + 1 >= (uint64_t{1} << 32) || ysum + 1 >= (uint64_t{1} << 32))
+      TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: tile offsets exceed 32 bits");
+    for (int leg : R) {
+      q.orow[row_of[leg]] = legs[leg].out_stride;
+      q.crow[row_of[leg]] = legs[leg].canon_stride;
+    }
+    for (int leg : yf) {
+      q.ocol[n_of[leg]] = legs[leg].out_stride;
+      q.ccol[n_of[leg]] = legs[leg].canon_stride;
+    }
+    return TNC_OK;
+  };
 
   auto* plan = new GatherTcPlan();
   std::memset(&plan->p, 0, sizeof(plan->p));
@@ -789,39 +887,9 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   plan->k = int64_t{1} << c;
   p.rbits = rb;
   p.fy = fy;
-  const uint32_t xatom = 128 * 128, yatom = static_cast<uint32_t>(nmma) * 128;
-  uint64_t xsum = 0, ysum = 0;
-  int j = 0;
-  for (int leg : xt) {
-    xsum += static_cast<uint64_t>(legs[leg].x_stride);
-    p.xg[j] = static_cast<uint32_t>(legs[leg].x_stride);
-    p.xs[j++] = legs[leg].kind == 0 ? row_bit_addr(row_of[leg]) : k_bit_addr(k_of[leg], xatom);
-  }
-  for (int r = rb; r < 7; ++r) {  // phantom rows: re-read rows, never stored
-    p.xg[j] = 0;
-    p.xs[j++] = row_bit_addr(r);
-  }
-  j = 0;
-  for (int leg : yt) {
-    ysum += static_cast<uint64_t>(legs[leg].y_stride);
-    p.yg[j] = static_cast<uint32_t>(legs[leg].y_stride);
-    p.ys[j++] = legs[leg].kind == 2 ? row_bit_addr(n_of[leg] + 1) : k_bit_addr(k_of[leg], yatom);
-  }
-  for (int n = fy; n < lgn; ++n) {  // phantom columns
-    p.yg[j] = 0;
-    p.ys[j++] = row_bit_addr(n + 1);
-  }
-  if (xsum >= (uint64_t{1} << 32) || ysum >= (uint64_t{1} << 32)) {
+  if (const int st = assign(false, false, p); st != TNC_OK) {
     delete plan;
-    TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: tile offsets exceed 32 bits");
-  }
-  for (int leg : R) {
-    p.orow[row_of[leg]] = legs[leg].out_stride;
-    p.crow[row_of[leg]] = legs[leg].canon_stride;
-  }
-  for (int leg : yf) {
-    p.ocol[n_of[leg]] = legs[leg].out_stride;
-    p.ccol[n_of[leg]] = legs[leg].canon_stride;
+    return st;
   }
   p.m_blocks = int64_t{1} << (fx - rb);
   p.kblocks = int64_t{1} << (c - kb);
@@ -879,6 +947,20 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   p.splits = splits;
   p.chunk_kb = std::max(1, 128 / kbc);  // 128 complex K per TMEM chain (as K2)
   if (const char* env = std::getenv("TNC_GT_CHUNK")) p.chunk_kb = std::max(1, std::atoi(env));
+  // paired layout: X's stride-1 leg is a tile common leg (it goes to k bit 0);
+  // Y pairs too when that leg is also Y's stride-1 leg.  Used at launch when
+  // the operand pointers are 16-byte aligned.
+  const bool px = legs[xt[0]].kind == 1 && legs[xt[0]].x_stride == 1;
+  // (not for 256-column tiles: the paired Y registers spill there, measured slower)
+  const bool py = px && nmma <= 128 && yt[0] == xt[0] && legs[yt[0]].y_stride == 1;
+  const char* pair_env = std::getenv("TNC_GT_PAIR");
+  if (px && !(pair_env && std::atoi(pair_env) == 0)) {
+    plan->p2 = p;
+    if (assign(true, py, plan->p2) == TNC_OK) {
+      plan->pair_x = true;
+      plan->pair_y = py;
+    }
+  }
   *out = plan;
   return TNC_OK;
 }
@@ -889,10 +971,10 @@ void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
 
 namespace {
 
-template <int NMMA, int KBC, int STAGES>
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
 int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
-  using Cfg = GtCfg<NMMA, KBC, STAGES>;
-  auto kern = gather_tc_kernel<NMMA, KBC, STAGES>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
   ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
@@ -913,7 +995,11 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
       TNC_CUDA_TRY(cudaMemcpy(plan->tabs_dev, plan->tabs_host.data(), bytes, cudaMemcpyHostToDevice));
     }
   }
-  GtParams p = plan->p;
+  // paired layout when the plan has one and the operands are 16-byte aligned
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                       (!plan->pair_y || (reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  const bool px = plan->pair_x && aligned, py = px && plan->pair_y;
+  GtParams p = px ? plan->p2 : plan->p;
   p.X = static_cast<const float2*>(x);
   p.Y = static_cast<const float2*>(y);
   p.C = static_cast<float2*>(c_final);
@@ -925,13 +1011,21 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
   const double M = static_cast<double>(plan->rows_x), N = static_cast<double>(plan->rows_y),
                K = static_cast<double>(plan->k);
   const double flops = 8.0 * M * N * K, bytes = 8.0 * (M * K + N * K + M * N);
+#define TNC_GT_CASE(N, KBC, ST)                                                        \
+  case N:                                                                              \
+    if (py) return launch_gt<N, KBC, ST, true, true>(p, units, flops, bytes, stream);  \
+    if (px) return launch_gt<N, KBC, ST, true, false>(p, units, flops, bytes, stream); \
+    return launch_gt<N, KBC, ST, false, false>(p, units, flops, bytes, stream);
   switch (plan->nmma) {
-    case 32: return launch_gt<32, 32, 2>(p, units, flops, bytes, stream);
-    case 64: return launch_gt<64, 32, 2>(p, units, flops, bytes, stream);
-    case 128: return launch_gt<128, 16, 3>(p, units, flops, bytes, stream);
-    case 256: return launch_gt<256, 16, 2>(p, units, flops, bytes, stream);
+    TNC_GT_CASE(32, 32, 2)
+    TNC_GT_CASE(64, 32, 2)
+    TNC_GT_CASE(128, 16, 3)
+    case 256:
+      if (px) return launch_gt<256, 16, 2, true, false>(p, units, flops, bytes, stream);
+      return launch_gt<256, 16, 2, false, false>(p, units, flops, bytes, stream);
     default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
   }
+#undef TNC_GT_CASE
 }
 
 }  // namespace tnc

@@ -144,3 +144,32 @@ def test_gather_tc_c1_full_size(cuda_ready, idx):
     assert [ix.label for ix in got.indices] == case.out_labels
     err = (got.flat().to(torch.complex128) - want).norm() / want.norm()
     assert err.item() <= TOL, (case.name, err.item())
+
+
+@pytest.mark.parametrize("fy,misaligned", [(4, False), (6, False), (7, False), (4, True)])
+def test_gather_tc_paired_layout(cuda_ready, fy, misaligned):
+    """X's and Y's stride-1 leg is the same common leg (as in C1c): the paired
+    16-byte layout runs (and, for a misaligned X view, the unpaired one)."""
+    from paper_2504_09186_b200 import DenseTensor, Index, contract_pair
+
+    rng = np.random.default_rng(40 + fy)
+    la = [f"x{i}" for i in range(10)] + [f"k{i}" for i in range(7)]
+    lb = [f"k{i}" for i in range(7)] + [f"y{i}" for i in range(fy)]
+    rng.shuffle(la)
+    rng.shuffle(lb)
+    for lst in (la, lb):  # k6 becomes the stride-1 leg of both operands
+        lst.remove("k6")
+        lst.append("k6")
+    da, db = _rand(rng, 2 ** len(la)), _rand(rng, 2 ** len(lb))
+    ta = torch.from_numpy(da).cuda()
+    if misaligned:  # 8-byte offset view: not 16-byte aligned
+        buf = torch.empty(da.size + 1, dtype=torch.complex64, device="cuda")
+        buf[1:] = ta
+        ta = buf[1:]
+    a = DenseTensor([Index(l) for l in la], ta.reshape([2] * len(la)))
+    b = DenseTensor([Index(l) for l in lb], db)
+    got = contract_pair(a, b, variant=TCGATHER)
+    want = tncref.contract((tuple(la), (2,) * len(la), da.astype(np.complex128)),
+                           (tuple(lb), (2,) * len(lb), db.astype(np.complex128)))
+    assert list(got.labels) == list(want[0])
+    assert rel_l2(got.numpy(), want[2]) <= TOL
