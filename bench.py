@@ -322,7 +322,9 @@ def bench_c3(args) -> None:
         e_s.record()
         d2h = 0
         for i in range(args.e2e_steps):
-            dev = [DenseTensor.__new__(DenseTensor)._init_raw(tt_.indices, hl.to("cuda", non_blocking=True))
+            # host-resident (pinned) leaves handed to the public API, which
+            # uploads them itself (one batched copy)
+            dev = [DenseTensor.__new__(DenseTensor)._init_raw(tt_.indices, hl)
                    for tt_, hl in zip(net.tensors, host_leaves)]
             if reuse_info is None:
                 amps = run_open(TensorNetwork(dev), t, spec, order, "single",

@@ -163,8 +163,16 @@ def _leaves_at(tensors: Sequence[DenseTensor], precision: str) -> list[DenseTens
     if not todo:
         return list(tensors)
     dev = torch.device("cuda", torch.cuda.current_device())
-    flat = torch.cat([tensors[i].data.reshape(-1).to(dev, non_blocking=True) for i in todo])
-    flat = flat.to(DTYPES[precision])
+    host = [i for i in todo if not tensors[i].data.is_cuda]
+    on_dev = [i for i in todo if tensors[i].data.is_cuda]
+    parts = []
+    if host:  # host-resident leaves: one host-side concatenation, one upload
+        hcat = torch.cat([tensors[i].data.reshape(-1) for i in host])
+        parts.append(hcat.to(dev, non_blocking=hcat.is_pinned()))
+    if on_dev:
+        parts.append(torch.cat([tensors[i].data.reshape(-1) for i in on_dev]))
+    todo = host + on_dev
+    flat = (parts[0] if len(parts) == 1 else torch.cat(parts)).to(DTYPES[precision])
     pos = 0
     for i in todo:
         t = tensors[i]
