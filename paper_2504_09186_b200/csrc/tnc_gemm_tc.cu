@@ -175,6 +175,42 @@ struct TcParams {
   const int* ey;         // 3xFP16: per-complex-column scale exponent of B
 };
 
+// 2^e as a float: exponent-field construction on the normal range, ldexpf
+// for the (rare) subnormal results
+__device__ __forceinline__ float pow2i(int e) {
+  return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.f, e);
+}
+
+// Undo the 3xFP16 per-row / per-column power-of-two operand scaling of one
+// thread's row segment (HALF fp32 = HALF/2 complex columns from ncol0).  The
+// column exponents come in as 16-byte vectors (ncol0 is a multiple of 4 and
+// the exponent array is 256-byte aligned); columns past N get exponent 0.
+template <int HALF>
+__device__ __forceinline__ void unscale(float (&acc)[HALF], const TcParams& p, int64_t row, int64_t ncol0) {
+  const int er = p.ex[row];
+  const int4* ey4 = reinterpret_cast<const int4*>(p.ey + ncol0);
+#pragma unroll
+  for (int q = 0; q < HALF / 8; ++q) {
+    int4 e = make_int4(0, 0, 0, 0);
+    if (ncol0 + 4 * q + 4 <= p.N) {
+      e = __ldg(ey4 + q);
+    } else {
+      if (ncol0 + 4 * q + 0 < p.N) e.x = p.ey[ncol0 + 4 * q + 0];
+      if (ncol0 + 4 * q + 1 < p.N) e.y = p.ey[ncol0 + 4 * q + 1];
+      if (ncol0 + 4 * q + 2 < p.N) e.z = p.ey[ncol0 + 4 * q + 2];
+    }
+    const float s0 = pow2i(er + e.x), s1 = pow2i(er + e.y), s2 = pow2i(er + e.z), s3 = pow2i(er + e.w);
+    acc[8 * q + 0] *= s0;
+    acc[8 * q + 1] *= s0;
+    acc[8 * q + 2] *= s1;
+    acc[8 * q + 3] *= s1;
+    acc[8 * q + 4] *= s2;
+    acc[8 * q + 5] *= s2;
+    acc[8 * q + 6] *= s3;
+    acc[8 * q + 7] *= s3;
+  }
+}
+
 template <int BN, int SWZ, int STAGES, bool F16>
 struct TcCfg {
   static constexpr int kElem = F16 ? 2 : 4;         // bytes per plane element
@@ -377,17 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sn = p.ldcn;
         }
         float2* drow = dst + row * sm;
-        if constexpr (F16) {
-          // undo the per-row / per-column power-of-two operand scaling
-          const int er = p.ex[row];
-#pragma unroll
-          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
-            const int64_t n = ncol0 + j;
-            const float s = ldexpf(1.f, er + (n < p.N ? p.ey[n] : 0));
-            acc[2 * j] *= s;
-            acc[2 * j + 1] *= s;
-          }
-        }
+        if constexpr (F16) unscale<Cfg::kHalf>(acc, p, row, ncol0);
         if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
           float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
 #pragma unroll
@@ -671,16 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           sn = p.ldcn;
         }
         float2* drow = dst + row * sm;
-        if constexpr (F16) {
-          const int er = p.ex[row];
-#pragma unroll
-          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
-            const int64_t n = ncol0 + j;
-            const float s = ldexpf(1.f, er + (n < p.N ? p.ey[n] : 0));
-            acc[2 * j] *= s;
-            acc[2 * j + 1] *= s;
-          }
-        }
+        if constexpr (F16) unscale<Cfg::kHalf>(acc, p, row, ncol0);
         if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
           float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
 #pragma unroll
