@@ -306,18 +306,24 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     TNC_CHECK_LAUNCH();
     return TNC_OK;
   }
-  // tile path: split long legs into factors <= 64 when possible
+  // tile path: split long legs.  Power-of-two legs (every quantum-circuit
+  // leg, and runs of them merged above) split into factors of 2, so the tile
+  // below can always grow one bit at a time to kMaxTile (with factors of 32 a
+  // merged run could stall the growth at a small tile, measured 2 TB/s on a
+  // C4 operand gather); other legs split into factors of 32 (a 32x32
+  // transpose tile still fits twice in kMaxTile)
   {
     std::vector<NormAxis> split;
     for (auto& a : ax) {
       NormAxis cur = a;
       std::vector<NormAxis> parts;  // least significant first
-      // factors of 32: a 32x32 transpose tile still fits twice in kMaxTile
-      while (cur.dim > 32 && cur.dim % 32 == 0) {
-        parts.push_back({32, cur.in_stride, cur.out_stride});
-        cur.in_stride *= 32;
-        cur.out_stride *= 32;
-        cur.dim /= 32;
+      const bool pow2 = (cur.dim & (cur.dim - 1)) == 0;
+      const int64_t f = pow2 ? 2 : 32;
+      while (cur.dim > f && cur.dim % f == 0) {
+        parts.push_back({f, cur.in_stride, cur.out_stride});
+        cur.in_stride *= f;
+        cur.out_stride *= f;
+        cur.dim /= f;
       }
       parts.push_back(cur);
       for (auto it = parts.rbegin(); it != parts.rend(); ++it) split.push_back(*it);
