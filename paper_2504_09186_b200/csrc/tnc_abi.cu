@@ -21,6 +21,7 @@
 
 #include "tnc_common.cuh"
 #include "tnc_gather_tc.cuh"
+#include "tnc_permute.cuh"
 
 namespace tnc {
 
@@ -728,9 +729,44 @@ static int prep_operand(const tnc_plan* p, const Operand& op, const void* src, u
   return TNC_OK;
 }
 
+// 3xFP16 plane pointers inside a plan's workspace
+struct F16Planes {
+  uint8_t *ab, *as, *bb, *bs;
+  int *ex, *ey;
+  void* scratch;
+};
+
+static F16Planes f16_planes(const tnc_plan* p, uint8_t* ws) {
+  const size_t a_plane = align_up(static_cast<size_t>(p->rows_x) * 2 * p->kp * 2);
+  const size_t b_plane = align_up(static_cast<size_t>(2 * p->rows_y) * 2 * p->kp * 2);
+  F16Planes f;
+  f.ab = ws + p->off_planes;
+  f.as = f.ab + a_plane;
+  f.bb = f.as + a_plane;
+  f.bs = f.bb + b_plane;
+  f.ex = reinterpret_cast<int*>(f.bs + b_plane);
+  f.ey = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(f.ex) + align_up(4 * p->rows_x));
+  f.scratch = reinterpret_cast<uint8_t*>(f.ey) + align_up(4 * p->rows_y);
+  return f;
+}
+
+// A gathered 3xFP16 operand goes straight from its own layout to the planes
+// (one tiled pass pair, no permuted copy) when K is a power of two >= 32.
+// Returns true when the planes were written.
+static bool fused_gather_split(const tnc_plan* p, const Operand& op, const void* src, int mode, int64_t rows,
+                               uint8_t* hi, uint8_t* lo, int* exps, void* scratch, cudaStream_t st) {
+  if (op.in_place || p->variant != TNC_VARIANT_TC3XF16 || p->kp != p->k || p->dtype != TNC_C64) return false;
+  if ((p->k & (p->k - 1)) != 0 || std::getenv("TNC_NO_FUSED_SPLIT")) return false;
+  int log_k = 0;
+  while ((int64_t{1} << log_k) < p->k) ++log_k;
+  return permute_split_f16_launch(static_cast<int>(op.dims.size()), op.dims.data(), op.strides.data(),
+                                  op.perm.data(), src, mode, rows, log_k, hi, lo, exps,
+                                  static_cast<unsigned*>(scratch), st) == TNC_OK;
+}
+
 static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* ym, int64_t ldy,
                     void* c, int64_t ldcm, int64_t ldcn, uint8_t* ws, int k_splits,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool x_planes_done = false, bool y_planes_done = false) {
   if (p->variant == TNC_VARIANT_TC3XTF32 || p->variant == TNC_VARIANT_TC3XF16) {
     const bool f16 = p->variant == TNC_VARIANT_TC3XF16;
     const size_t pe = f16 ? 2 : 4;
@@ -744,8 +780,8 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     int* ey = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ex) + align_up(4 * p->rows_x));
     if (f16) {
       void* scratch = reinterpret_cast<uint8_t*>(ey) + align_up(4 * p->rows_y);
-      TNC_TRY(f16_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, ex, scratch, st));
-      TNC_TRY(f16_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, ey, scratch, st));
+      if (!x_planes_done) TNC_TRY(f16_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, ex, scratch, st));
+      if (!y_planes_done) TNC_TRY(f16_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, ey, scratch, st));
     } else {
       TNC_TRY(tf32_split_launch(0, p->rows_x, p->k, p->kp, xm, ldx, ab, as, st));
       TNC_TRY(tf32_split_launch(1, p->rows_y, p->k, p->kp, ym, ldy, bb, bs, st));
@@ -796,12 +832,18 @@ int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void*
                              p->out_perm_strides.data(), p->out_perm.data(), dst, c, st));
     return TNC_OK;
   }
-  const void *xm, *ym;
-  int64_t ldx, ldy;
-  TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
-  TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
+  const void *xm = nullptr, *ym = nullptr;
+  int64_t ldx = 0, ldy = 0;
+  bool x_done = false, y_done = false;
+  if (p->variant == TNC_VARIANT_TC3XF16) {
+    const F16Planes f = f16_planes(p, ws);
+    x_done = fused_gather_split(p, p->x, xsrc, 0, p->rows_x, f.ab, f.as, f.ex, f.scratch, st);
+    y_done = fused_gather_split(p, p->y, ysrc, 1, p->rows_y, f.bb, f.bs, f.ey, f.scratch, st);
+  }
+  if (!x_done) TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
+  if (!y_done) TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
   void* dst = p->custom_out ? static_cast<void*>(ws + p->off_tmp) : c;
-  TNC_TRY(run_gemm(p, xm, ldx, ym, ldy, dst, p->ldcm, p->ldcn, ws, p->k_splits, st));
+  TNC_TRY(run_gemm(p, xm, ldx, ym, ldy, dst, p->ldcm, p->ldcn, ws, p->k_splits, st, x_done, y_done));
   if (p->custom_out) {
     TNC_TRY(permute_launch(p->dtype, static_cast<int>(p->out_perm.size()),
                            p->out_perm_dims.data(), p->out_perm_strides.data(),

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "tnc_common.cuh"
+#include "tnc_permute.cuh"
 
 namespace tnc {
 
@@ -88,30 +89,59 @@ __device__ __forceinline__ int pad_idx(int e) { return e + (e >> 4); }
 constexpr int kTileThreads = 256;
 constexpr int kItems = kMaxTile / kTileThreads;  // elements per thread per tile (<= 8)
 
-template <typename T>
+// Epilogue of the tile kernel: a plain copy, or the 3xFP16 operand split of a
+// GEMM operand gathered to [R rows, K] (K = 2^log_k, row pitch K): pass 1
+// (ROWMAX) folds each row's max |component| into rowmax[], pass 2 (SPLIT0 /
+// SPLIT1) writes the scaled hi / lo fp16 planes (SPLIT1: the expanded rows
+// 2r = (re, -im), 2r+1 = (im, re)) -- the same planes f16_split_launch makes
+// from the permuted copy, without writing or re-reading that copy.
+enum PermMode { PERM_COPY = 0, PERM_ROWMAX = 1, PERM_SPLIT0 = 2, PERM_SPLIT1 = 3 };
+
+struct SplitOut {
+  int log_k;
+  unsigned* rowmax;   // ROWMAX: float bits of max |component| per row (atomicMax)
+  const float* scale; // SPLIT: per-row 2^-e
+  __half2* hi;
+  __half2* lo;
+};
+
+template <typename T, int MODE>
 __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __restrict__ in,
                                                                     T* __restrict__ out,
-                                                                    const PermParams p) {
+                                                                    const PermParams p, const SplitOut so_) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tiles_pad = pad_idx(p.tile_elems) + 1;
   int64_t* in_off = reinterpret_cast<int64_t*>(tile + tiles_pad);
   int64_t* out_off = in_off + p.tile_elems;
   int* src_of = reinterpret_cast<int*>(out_off + p.tile_elems);
+  // ROWMAX only: row slot of each input-order element, per-slot maxima
+  int16_t* slot_of = reinterpret_cast<int16_t*>(src_of + p.tile_elems);
+  unsigned* rmax = reinterpret_cast<unsigned*>(slot_of + p.tile_elems + (p.tile_elems & 1));
   __shared__ int64_t s_base[2];
+  __shared__ int s_nslots;
 
   // Build tables once per block.
   // Input-order enumeration e: digits over tile axes, axis 0 fastest.
   // Output-order enumeration f: digits ordered by tile_out_rank (0 fastest).
   for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) {
     int64_t rem = e, oin = 0;
+    int slot = 0, cm = 1;
     for (int a = 0; a < p.n_tile; ++a) {
       int64_t d = p.tile_dim[a];
       int64_t q = rem / d;
       oin += (rem - q * d) * p.tile_in[a];
+      if (MODE == PERM_ROWMAX && p.tile_out[a] >= (int64_t{1} << so_.log_k)) {  // a row axis
+        slot += static_cast<int>(rem - q * d) * cm;
+        cm *= static_cast<int>(d);
+      }
       rem = q;
     }
     in_off[e] = oin;
+    if (MODE == PERM_ROWMAX) {
+      slot_of[e] = static_cast<int16_t>(slot);
+      if (e == 0) s_nslots = cm;
+    }
   }
   for (int f = threadIdx.x; f < p.tile_elems; f += blockDim.x) {
     // decode f over axes sorted by output stride (rank 0 fastest)
@@ -163,6 +193,35 @@ __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __r
       const int e = tid + i * kTileThreads;
       if (e < p.tile_elems) v[i] = src[in_off[e]];
     }
+    if constexpr (MODE == PERM_ROWMAX) {
+      // per-tile row maxima in smem (no transpose needed), then one global
+      // atomic per row of the tile; non-negative floats order like their bits
+      for (int q = tid; q < s_nslots; q += kTileThreads) rmax[q] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int e = tid + i * kTileThreads;
+        if (e < p.tile_elems) {
+          // a tile can hold few rows: read first, so only increases hit the
+          // (contended) smem atomic
+          const unsigned b = __float_as_uint(fmaxf(fabsf(v[i].re), fabsf(v[i].im)));
+          volatile unsigned* a = rmax + slot_of[e];
+          if (b > *a) atomicMax(const_cast<unsigned*>(a), b);
+        }
+      }
+      __syncthreads();
+      for (int q = tid; q < s_nslots; q += kTileThreads) {
+        int64_t off = 0;
+        int rest = q;
+        for (int a = 0; a < p.n_tile; ++a)
+          if (p.tile_out[a] >= (int64_t{1} << so_.log_k)) {
+            off += static_cast<int64_t>(rest % p.tile_dim[a]) * p.tile_out[a];
+            rest /= static_cast<int>(p.tile_dim[a]);
+          }
+        atomicMax(so_.rowmax + ((s_base[1] + off) >> so_.log_k), rmax[q]);
+      }
+      __syncthreads();
+    } else {
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const int e = tid + i * kTileThreads;
@@ -174,12 +233,180 @@ __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __r
       const int f = tid + i * kTileThreads;
       if (f < p.tile_elems) v[i] = tile[src_of[f]];
     }
+    if constexpr (MODE == PERM_COPY) {
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const int f = tid + i * kTileThreads;
-      if (f < p.tile_elems) dst[out_off[f]] = v[i];
+      for (int i = 0; i < kItems; ++i) {
+        const int f = tid + i * kTileThreads;
+        if (f < p.tile_elems) dst[out_off[f]] = v[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const int f = tid + i * kTileThreads;
+        if (f < p.tile_elems) {
+          const int64_t o = s_base[1] + out_off[f];
+          const int64_t r = o >> so_.log_k;
+          const int64_t k = o & ((int64_t{1} << so_.log_k) - 1);
+          const float sc = __ldg(so_.scale + r);
+          const float re = v[i].re * sc, im = v[i].im * sc;
+          const __half hre = __float2half_rn(re), him = __float2half_rn(im);
+          const __half lre = __float2half_rn(re - __half2float(hre));
+          const __half lim = __float2half_rn(im - __half2float(him));
+          if constexpr (MODE == PERM_SPLIT0) {
+            so_.hi[o] = __halves2half2(hre, him);
+            so_.lo[o] = __halves2half2(lre, lim);
+          } else {
+            const int64_t o0 = ((2 * r) << so_.log_k) + k;
+            const int64_t o1 = o0 + (int64_t{1} << so_.log_k);
+            so_.hi[o0] = __halves2half2(hre, __hneg(him));
+            so_.lo[o0] = __halves2half2(lre, __hneg(lim));
+            so_.hi[o1] = __halves2half2(him, hre);
+            so_.lo[o1] = __halves2half2(lim, lre);
+          }
+        }
+      }
     }
     __syncthreads();
+    }  // MODE != PERM_ROWMAX
+  }
+}
+
+// Row maxima of a permuted view without permuting it.  The operand's legs are
+// all powers of two, so the view splits into binary axes; each is a row axis
+// (output stride >= 2^log_k) or a K axis.  The five smallest-input-stride axes
+// are the lane bits (one coalesced 256-byte load per warp instruction); the
+// other K axes are walked by a carry-delta counter; the other row axes pick
+// the warp's task.  A task keeps its rows' maxima in registers, folds the lanes
+// that differ only in K bits with shuffles, and does one global atomicMax per
+// row -- the tile kernel's ROWMAX mode paid per-tile smem atomics plus one
+// global atomic per tile row (~2 TB/s on C3's operands).
+constexpr int kRmAxes = 40;
+struct RowmaxParams {
+  int64_t lane_in[5];
+  int64_t lane_row[5];
+  unsigned lane_kmask;      // lane bits that are K axes
+  int n_ro;                 // row axes outside the lanes
+  int kc_log;               // K-walk length per task: 2^kc_log
+  int chunk_bits;           // (n K axes outside the lanes) - kc_log
+  int64_t tasks;
+  int64_t ro_in[kRmAxes];
+  int64_t ro_row[kRmAxes];
+  int64_t ko_in[kRmAxes];     // K axes outside the lanes, fastest first
+  int64_t ko_delta[kRmAxes + 1];  // off(j + 1) - off(j) when ctz(j + 1) = t
+};
+
+__global__ void __launch_bounds__(256) rowmax_warp_kernel(const c64* __restrict__ in, const RowmaxParams p,
+                                                          unsigned* __restrict__ rowmax) {
+  const int lane = threadIdx.x & 31;
+  int64_t lane_off = 0, lane_row = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b)
+    if ((lane >> b) & 1) {
+      lane_off += p.lane_in[b];
+      lane_row += p.lane_row[b];
+    }
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t steps = int64_t{1} << p.kc_log;
+  for (int64_t task = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); task < p.tasks;
+       task += nw) {
+    const int64_t ro = task >> p.chunk_bits;
+    int64_t base = lane_off, row = lane_row;
+    for (int b = 0; b < p.n_ro; ++b)
+      if ((ro >> b) & 1) {
+        base += p.ro_in[b];
+        row += p.ro_row[b];
+      }
+    const int64_t kc = task & ((int64_t{1} << p.chunk_bits) - 1);
+    for (int b = 0; b < p.chunk_bits; ++b)
+      if ((kc >> b) & 1) base += p.ko_in[p.kc_log + b];
+    const float2* src = reinterpret_cast<const float2*>(in) + base;
+    float m = 0.f;
+    int64_t off = 0;
+    for (int64_t j = 0; j < steps; j += 8) {
+      int64_t o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        o[u] = off;
+        off += p.ko_delta[__ffsll(j + u + 1) - 1];
+      }
+      float2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < steps) v[u] = __ldg(src + o[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < steps) m = fmaxf(m, fmaxf(fabsf(v[u].x), fabsf(v[u].y)));
+    }
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+      if ((p.lane_kmask >> b) & 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1 << b));
+    // non-negative floats order like their bit patterns (NaN sorts above all)
+    if ((lane & p.lane_kmask) == 0) atomicMax(rowmax + row, __float_as_uint(m));
+  }
+}
+
+// false when the view does not fit the binary-axis scheme (the tile kernel's
+// ROWMAX mode then runs)
+bool plan_rowmax(int rank, const int64_t* dims, const int64_t* in_strides, const int32_t* perm, int log_k,
+                 int sms, RowmaxParams& p, int64_t& blocks) {
+  struct Bit {
+    int64_t in, out;
+  };
+  std::vector<Bit> bits;
+  int64_t os = 1;
+  for (int t = rank - 1; t >= 0; --t) {
+    const int s = perm[t];
+    const int64_t d = dims[s];
+    if (d < 1 || (d & (d - 1)) != 0) return false;
+    for (int64_t f = 1; f < d; f *= 2) bits.push_back({in_strides[s] * f, os * f});
+    os *= d;
+  }
+  if (bits.size() < 5 || bits.size() > static_cast<size_t>(kRmAxes)) return false;
+  std::stable_sort(bits.begin(), bits.end(), [](const Bit& a, const Bit& b) { return a.in < b.in; });
+  const int64_t K = int64_t{1} << log_k;
+  p = RowmaxParams{};
+  std::vector<int64_t> ko;
+  for (size_t i = 0; i < bits.size(); ++i) {
+    const bool is_row = bits[i].out >= K;
+    if (i < 5) {
+      p.lane_in[i] = bits[i].in;
+      p.lane_row[i] = is_row ? bits[i].out >> log_k : 0;
+      if (!is_row) p.lane_kmask |= 1u << i;
+    } else if (is_row) {
+      p.ro_in[p.n_ro] = bits[i].in;
+      p.ro_row[p.n_ro] = bits[i].out >> log_k;
+      ++p.n_ro;
+    } else {
+      ko.push_back(bits[i].in);
+    }
+  }
+  const int n_ko = static_cast<int>(ko.size());
+  int64_t sum = 0;
+  for (int t = 0; t < n_ko; ++t) {
+    p.ko_in[t] = ko[t];
+    p.ko_delta[t] = ko[t] - sum;
+    sum += ko[t];
+  }
+  // enough tasks to fill every SM several times over, >= 8 steps per task
+  const int64_t warps = static_cast<int64_t>(sms) * 64;
+  p.kc_log = n_ko;
+  while (p.kc_log > 3 && (int64_t{1} << (p.n_ro + n_ko - p.kc_log)) < 8 * warps) --p.kc_log;
+  p.chunk_bits = n_ko - p.kc_log;
+  p.tasks = int64_t{1} << (p.n_ro + p.chunk_bits);
+  blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.tasks, 8), static_cast<int64_t>(sms) * 8));
+  return true;
+}
+
+// row maxima -> exponents (for the GEMM epilogue) and 2^-e scales (written
+// over the maxima: the split pass reads them as floats)
+__global__ void rowmax_to_exp_kernel(int64_t R, unsigned* __restrict__ rowmax, int* __restrict__ exps) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < R;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float mx = __uint_as_float(rowmax[r]);
+    int e = 0;
+    if (mx > 0.f && isfinite(mx)) frexpf(mx, &e);  // same rule as f16_split_kernel
+    exps[r] = e;
+    rowmax[r] = __float_as_uint(ldexpf(1.f, -e));
   }
 }
 
@@ -231,8 +458,21 @@ int fill_outer(const std::vector<NormAxis>& axes, OuterAxes& o) {
 
 }  // namespace
 
-int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
-                   const int32_t* perm, const void* in, void* out, cudaStream_t stream) {
+namespace {
+
+// How a permutation runs: a plain copy, one contiguous run per output row, or
+// smem tiles (see the file header).
+struct PermPlan {
+  enum Kind { EMPTY, MEMCPY, ROWS, TILE } kind = EMPTY;
+  int64_t total = 0;
+  RowParams rp{};
+  PermParams tp{};
+  int64_t blocks = 0;
+  size_t smem = 0;
+};
+
+int plan_permute(size_t eb, int rank, const int64_t* dims, const int64_t* in_strides, const int32_t* perm,
+                 PermPlan& pl) {
   if (rank < 0 || rank > TNC_MAX_RANK) TNC_RET(TNC_ERR_TENSOR, "permute: rank out of range");
   std::vector<int> seen(rank, 0);
   int64_t total = 1;
@@ -245,7 +485,7 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     if (dims[s] < 1) TNC_RET(TNC_ERR_TENSOR, "permute: dim < 1");
     total *= dims[s];
   }
-  const size_t eb = elem_bytes(dtype);
+  pl.total = total;
   // target-order axes with output strides (contiguous output)
   std::vector<NormAxis> ax;
   {
@@ -277,33 +517,26 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     }
     ax.swap(merged);
   }
-  if (total == 0) return TNC_OK;
-  ProfScope prof(PROF_PERMUTE, 0.0, 2.0 * static_cast<double>(total) * eb, stream);
+  if (total == 0) {
+    pl.kind = PermPlan::EMPTY;
+    return TNC_OK;
+  }
   // full contiguous copy
   if (ax.empty() || (ax.size() == 1 && ax[0].in_stride == 1)) {
-    TNC_CUDA_TRY(cudaMemcpyAsync(out, in, static_cast<size_t>(total) * eb,
-                                 cudaMemcpyDeviceToDevice, stream));
+    pl.kind = PermPlan::MEMCPY;
     return TNC_OK;
   }
   const int sms = num_sms();
   // row copy when the innermost output leg is unit stride in the input and long
   const NormAxis& inner = ax.back();
   if (inner.in_stride == 1 && inner.dim >= 16) {
-    RowParams p{};
+    RowParams& p = pl.rp;
     p.row_len = inner.dim;
     p.n_rows = total / inner.dim;
     std::vector<NormAxis> outer(ax.begin(), ax.end() - 1);
     TNC_TRY(fill_outer(outer, p.outer));
-    int64_t warps_needed = p.n_rows;
-    int64_t blocks = std::min<int64_t>(ceil_div(warps_needed, 8), static_cast<int64_t>(sms) * 16);
-    blocks = std::max<int64_t>(blocks, 1);
-    if (dtype == TNC_C128)
-      permute_rows_kernel<c128><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-          static_cast<const c128*>(in), static_cast<c128*>(out), p);
-    else
-      permute_rows_kernel<c64><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-          static_cast<const c64*>(in), static_cast<c64*>(out), p);
-    TNC_CHECK_LAUNCH();
+    pl.blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(p.n_rows, 8), static_cast<int64_t>(sms) * 16), 1);
+    pl.kind = PermPlan::ROWS;
     return TNC_OK;
   }
   // tile path: split long legs.  Power-of-two legs (every quantum-circuit
@@ -398,7 +631,7 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     tile = ax[by_out[0]].dim;
     if (tile > kMaxTile) TNC_RET(TNC_ERR_UNSUPPORTED, "permute: unsplittable leg too long");
   }
-  PermParams p{};
+  PermParams& p = pl.tp;
   p.tile_elems = static_cast<int>(tile);
   int nt = 0;
   for (int a : by_in)
@@ -426,18 +659,88 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
   const int tiles_pad = (p.tile_elems + (p.tile_elems >> 4)) + 1;
   size_t smem = static_cast<size_t>(tiles_pad) * eb + static_cast<size_t>(p.tile_elems) * 20;
   smem = (smem + 15) & ~size_t(15);
-  int blocks_per_sm = tile >= 1024 ? 3 : 6;
-  int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(sms) * blocks_per_sm);
+  const int blocks_per_sm = tile >= 1024 ? 3 : 6;
+  pl.blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(sms) * blocks_per_sm);
+  pl.smem = smem;
+  pl.kind = PermPlan::TILE;
+  return TNC_OK;
+}
+
+}  // namespace
+
+int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
+                   const int32_t* perm, const void* in, void* out, cudaStream_t stream) {
+  const size_t eb = elem_bytes(dtype);
+  PermPlan pl;
+  TNC_TRY(plan_permute(eb, rank, dims, in_strides, perm, pl));
+  if (pl.kind == PermPlan::EMPTY) return TNC_OK;
+  ProfScope prof(PROF_PERMUTE, 0.0, 2.0 * static_cast<double>(pl.total) * eb, stream);
+  if (pl.kind == PermPlan::MEMCPY) {
+    TNC_CUDA_TRY(cudaMemcpyAsync(out, in, static_cast<size_t>(pl.total) * eb, cudaMemcpyDeviceToDevice, stream));
+    return TNC_OK;
+  }
+  if (pl.kind == PermPlan::ROWS) {
+    if (dtype == TNC_C128)
+      permute_rows_kernel<c128><<<static_cast<unsigned>(pl.blocks), 256, 0, stream>>>(
+          static_cast<const c128*>(in), static_cast<c128*>(out), pl.rp);
+    else
+      permute_rows_kernel<c64><<<static_cast<unsigned>(pl.blocks), 256, 0, stream>>>(
+          static_cast<const c64*>(in), static_cast<c64*>(out), pl.rp);
+    TNC_CHECK_LAUNCH();
+    return TNC_OK;
+  }
+  const SplitOut none{};
   if (dtype == TNC_C128) {
-    auto k = permute_tile_kernel<c128>;
+    auto k = permute_tile_kernel<c128, PERM_COPY>;
     TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(static_cast<const c128*>(in),
-                                                            static_cast<c128*>(out), p);
+    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c128*>(in),
+                                                                  static_cast<c128*>(out), pl.tp, none);
   } else {
-    auto k = permute_tile_kernel<c64>;
+    auto k = permute_tile_kernel<c64, PERM_COPY>;
     TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(static_cast<const c64*>(in),
-                                                            static_cast<c64*>(out), p);
+    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in),
+                                                                  static_cast<c64*>(out), pl.tp, none);
+  }
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
+
+int permute_split_f16_launch(int rank, const int64_t* dims, const int64_t* in_strides, const int32_t* perm,
+                             const void* in, int mode, int64_t R, int log_k, void* hi, void* lo, int* exps,
+                             unsigned* rowmax, cudaStream_t stream) {
+  PermPlan pl;
+  TNC_TRY(plan_permute(sizeof(c64), rank, dims, in_strides, perm, pl));
+  if (pl.kind != PermPlan::TILE) TNC_RET(TNC_ERR_UNSUPPORTED, "permute+split: not a tiled permutation");
+  if (pl.total != (R << log_k)) TNC_RET(TNC_ERR_INVALID, "permute+split: R * 2^log_k != elements");
+  // one read for the row maxima, one read + the plane writes for the split
+  ProfScope prof(PROF_SPLIT_PREP, 0.0, 16.0 * pl.total + (mode ? 16.0 : 8.0) * pl.total, stream);
+  TNC_CUDA_TRY(cudaMemsetAsync(rowmax, 0, static_cast<size_t>(R) * sizeof(unsigned), stream));
+  SplitOut so{log_k, rowmax, reinterpret_cast<const float*>(rowmax), static_cast<__half2*>(hi),
+              static_cast<__half2*>(lo)};
+  RowmaxParams rp;
+  int64_t rblocks = 0;
+  if (std::getenv("TNC_TILE_ROWMAX") == nullptr &&
+      plan_rowmax(rank, dims, in_strides, perm, log_k, num_sms(), rp, rblocks)) {
+    rowmax_warp_kernel<<<static_cast<unsigned>(rblocks), 256, 0, stream>>>(static_cast<const c64*>(in), rp, rowmax);
+    TNC_CHECK_LAUNCH();
+  } else {
+    auto k = permute_tile_kernel<c64, PERM_ROWMAX>;
+    const size_t smem = pl.smem + static_cast<size_t>(pl.tp.tile_elems) * (2 + 4) + 16;
+    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    k<<<static_cast<unsigned>(pl.blocks), 256, smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
+    TNC_CHECK_LAUNCH();
+  }
+  rowmax_to_exp_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(R, 256), 4096))), 256,
+                         0, stream>>>(R, rowmax, exps);
+  TNC_CHECK_LAUNCH();
+  if (mode == 0) {
+    auto k = permute_tile_kernel<c64, PERM_SPLIT0>;
+    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
+  } else {
+    auto k = permute_tile_kernel<c64, PERM_SPLIT1>;
+    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
   }
   TNC_CHECK_LAUNCH();
   return TNC_OK;
