@@ -105,15 +105,17 @@ struct SplitOut {
   __half2* lo;
 };
 
-template <typename T, int MODE>
+// Off: element offsets inside one tile, int32 when every tile offset fits
+// (smaller tables: 4 instead of 3 blocks per SM for complex64 tiles)
+template <typename T, int MODE, typename Off>
 __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __restrict__ in,
                                                                     T* __restrict__ out,
                                                                     const PermParams p, const SplitOut so_) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tiles_pad = pad_idx(p.tile_elems) + 1;
-  int64_t* in_off = reinterpret_cast<int64_t*>(tile + tiles_pad);
-  int64_t* out_off = in_off + p.tile_elems;
+  Off* in_off = reinterpret_cast<Off*>(tile + tiles_pad);
+  Off* out_off = in_off + p.tile_elems;
   int* src_of = reinterpret_cast<int*>(out_off + p.tile_elems);
   // ROWMAX only: row slot of each input-order element, per-slot maxima
   int16_t* slot_of = reinterpret_cast<int16_t*>(src_of + p.tile_elems);
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __r
       }
       rem = q;
     }
-    in_off[e] = oin;
+    in_off[e] = static_cast<Off>(oin);
     if (MODE == PERM_ROWMAX) {
       slot_of[e] = static_cast<int16_t>(slot);
       if (e == 0) s_nslots = cm;
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kTileThreads) permute_tile_kernel(const T* __r
       e += static_cast<int>(digit[a] * mul);
       mul *= p.tile_dim[a];
     }
-    out_off[f] = oout;
+    out_off[f] = static_cast<Off>(oout);
     src_of[f] = pad_idx(e);
   }
   __syncthreads();
@@ -469,6 +471,7 @@ struct PermPlan {
   PermParams tp{};
   int64_t blocks = 0;
   size_t smem = 0;
+  bool off32 = false;  // tile offset tables fit int32
 };
 
 int plan_permute(size_t eb, int rank, const int64_t* dims, const int64_t* in_strides, const int32_t* perm,
@@ -657,9 +660,19 @@ int plan_permute(size_t eb, int rank, const int64_t* dims, const int64_t* in_str
   }
   p.n_tiles = total / tile;
   const int tiles_pad = (p.tile_elems + (p.tile_elems >> 4)) + 1;
-  size_t smem = static_cast<size_t>(tiles_pad) * eb + static_cast<size_t>(p.tile_elems) * 20;
+  {
+    int64_t max_in = 0, max_out = 0;
+    for (int a = 0; a < p.n_tile; ++a) {
+      max_in += (p.tile_dim[a] - 1) * p.tile_in[a];
+      max_out += (p.tile_dim[a] - 1) * p.tile_out[a];
+    }
+    pl.off32 = max_in <= INT32_MAX && max_out <= INT32_MAX;
+  }
+  size_t smem = static_cast<size_t>(tiles_pad) * eb + static_cast<size_t>(p.tile_elems) * (pl.off32 ? 12 : 20);
   smem = (smem + 15) & ~size_t(15);
-  const int blocks_per_sm = tile >= 1024 ? 3 : 6;
+  // residency by smem (+ ~4.5 KB of static tables per block)
+  const int by_smem = static_cast<int>((200 * 1024) / (smem + 4608));
+  const int blocks_per_sm = std::max(1, std::min(tile >= 1024 ? 4 : 6, by_smem));
   pl.blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(sms) * blocks_per_sm);
   pl.smem = smem;
   pl.kind = PermPlan::TILE;
@@ -667,6 +680,18 @@ int plan_permute(size_t eb, int rank, const int64_t* dims, const int64_t* in_str
 }
 
 }  // namespace
+
+// launch the tile kernel with the offset width the plan allows
+template <typename T, int MODE>
+int launch_tile(const PermPlan& pl, const void* in, void* out, const SplitOut& so, size_t smem,
+                cudaStream_t stream) {
+  auto k = pl.off32 ? permute_tile_kernel<T, MODE, int32_t> : permute_tile_kernel<T, MODE, int64_t>;
+  TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  k<<<static_cast<unsigned>(pl.blocks), 256, smem, stream>>>(static_cast<const T*>(in), static_cast<T*>(out),
+                                                             pl.tp, so);
+  TNC_CHECK_LAUNCH();
+  return TNC_OK;
+}
 
 int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
                    const int32_t* perm, const void* in, void* out, cudaStream_t stream) {
@@ -690,19 +715,8 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     return TNC_OK;
   }
   const SplitOut none{};
-  if (dtype == TNC_C128) {
-    auto k = permute_tile_kernel<c128, PERM_COPY>;
-    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c128*>(in),
-                                                                  static_cast<c128*>(out), pl.tp, none);
-  } else {
-    auto k = permute_tile_kernel<c64, PERM_COPY>;
-    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in),
-                                                                  static_cast<c64*>(out), pl.tp, none);
-  }
-  TNC_CHECK_LAUNCH();
-  return TNC_OK;
+  if (dtype == TNC_C128) return launch_tile<c128, PERM_COPY>(pl, in, out, none, pl.smem, stream);
+  return launch_tile<c64, PERM_COPY>(pl, in, out, none, pl.smem, stream);
 }
 
 int permute_split_f16_launch(int rank, const int64_t* dims, const int64_t* in_strides, const int32_t* perm,
@@ -724,26 +738,14 @@ int permute_split_f16_launch(int rank, const int64_t* dims, const int64_t* in_st
     rowmax_warp_kernel<<<static_cast<unsigned>(rblocks), 256, 0, stream>>>(static_cast<const c64*>(in), rp, rowmax);
     TNC_CHECK_LAUNCH();
   } else {
-    auto k = permute_tile_kernel<c64, PERM_ROWMAX>;
     const size_t smem = pl.smem + static_cast<size_t>(pl.tp.tile_elems) * (2 + 4) + 16;
-    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(pl.blocks), 256, smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
-    TNC_CHECK_LAUNCH();
+    TNC_TRY((launch_tile<c64, PERM_ROWMAX>(pl, in, nullptr, so, smem, stream)));
   }
   rowmax_to_exp_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(R, 256), 4096))), 256,
                          0, stream>>>(R, rowmax, exps);
   TNC_CHECK_LAUNCH();
-  if (mode == 0) {
-    auto k = permute_tile_kernel<c64, PERM_SPLIT0>;
-    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
-  } else {
-    auto k = permute_tile_kernel<c64, PERM_SPLIT1>;
-    TNC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    k<<<static_cast<unsigned>(pl.blocks), 256, pl.smem, stream>>>(static_cast<const c64*>(in), nullptr, pl.tp, so);
-  }
-  TNC_CHECK_LAUNCH();
-  return TNC_OK;
+  if (mode == 0) return launch_tile<c64, PERM_SPLIT0>(pl, in, nullptr, so, pl.smem, stream);
+  return launch_tile<c64, PERM_SPLIT1>(pl, in, nullptr, so, pl.smem, stream);
 }
 
 }  // namespace tnc
