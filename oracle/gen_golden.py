@@ -8,7 +8,7 @@ travel instead.
 
     python oracle/gen_golden.py [section ...]
 
-Sections: perm contract split c0 plans sliced reuse pairs spill
+Sections: perm contract split c0 plans sliced reuse pairs spill plan_c4_reuse
 """
 
 from __future__ import annotations
@@ -283,6 +283,16 @@ def section_plans():
     _dump("plan_c4", _plan_fixture(workloads.C4, workloads.C4_MAX_RANK, False))
 
 
+def section_plan_c4_reuse():
+    """C4 spindle plan at the reference's default max_k = 12 (12 nested labels,
+    21 outer, ~34k actions, ~118 GiB predicted peak).  Slow: the reference
+    planner takes several minutes here."""
+    obj = _plan_fixture(workloads.C4, workloads.C4_MAX_RANK, True, max_k=12)
+    keep = {k: obj[k] for k in ("rows", "cols", "cycles", "seed", "open", "max_rank")}
+    keep["reuse"] = obj["reuse"]
+    _dump("plan_c4_reuse", keep)
+
+
 def section_sliced():
     """Small end-to-end sliced + reuse runs with full data (oracle-sized)."""
     wl = workloads.CircuitWorkload(4, 4, 10, 3, 3)
@@ -407,7 +417,7 @@ def section_spill():
 SECTIONS = {
     "perm": section_perm, "contract": section_contract, "split": section_split, "c0": section_c0,
     "plans": section_plans, "sliced": section_sliced, "reuse": section_reuse, "pairs": section_pairs,
-    "spill": section_spill,
+    "spill": section_spill, "plan_c4_reuse": section_plan_c4_reuse,
 }
 
 if __name__ == "__main__":

@@ -32,7 +32,7 @@ def _prod(xs) -> int:
     return out
 
 
-# -- reference tensor.py:318-352 ------------------------------------------------
+# -- reference tensor.py:182-249 (PermutationPlan, _case_bucket, classify_permutation) --
 def classify(src: Sequence[tuple[str, int]], tgt: Sequence[tuple[str, int]]):
     """(stride, offset, case, chunk, src_step) of reordering src -> tgt."""
     if sorted(src) != sorted(tgt):
@@ -61,7 +61,7 @@ def classify(src: Sequence[tuple[str, int]], tgt: Sequence[tuple[str, int]]):
     return (stride, offset, case, chunk, src_step)
 
 
-# -- reference tensor.py:355-377 (offset table + gather) --------------------------
+# -- reference tensor.py:252-274 (permute: offset table + gather) --
 def permute(t: Tensor, target: Sequence[str]) -> Tensor:
     labels, dims, data = t
     dim_of = dict(zip(labels, dims))
@@ -82,7 +82,7 @@ def permute(t: Tensor, target: Sequence[str]) -> Tensor:
     return (tuple(target), tuple(d for _, d in tgt), data[offsets])
 
 
-# -- reference tensor.py:380-395 --------------------------------------------------
+# -- reference tensor.py:277-292 (project) --
 def project(t: Tensor, assignment: dict[str, int]) -> Tensor:
     labels, dims, data = t
     if not any(l in assignment for l in labels):
@@ -93,7 +93,7 @@ def project(t: Tensor, assignment: dict[str, int]) -> Tensor:
     return (tuple(l for l, _ in kept), tuple(d for _, d in kept), arr)
 
 
-# -- reference contract.py:58-117 -------------------------------------------------
+# -- reference contract.py:58-117 (_split_legs, contraction_shape, ttgt_plan) --
 def ttgt(a_labels, a_dims, b_labels, b_dims):
     bdim = dict(zip(b_labels, b_dims))
     free_a, common = [], []
@@ -122,7 +122,7 @@ def ttgt(a_labels, a_dims, b_labels, b_dims):
     return free_a, common, free_b, (m, k, n), b_mult, a_tgt, b_tgt
 
 
-# -- reference contract.py:131-165 ------------------------------------------------
+# -- reference contract.py:131-165 (_matmul, _panel_product, _finish, contract_pair) --
 def _operands(a: Tensor, b: Tensor):
     free_a, common, free_b, (m, k, n), b_mult, a_tgt, b_tgt = ttgt(a[0], a[1], b[0], b[1])
     a2 = permute(a, [l for l, _ in a_tgt])[2]
@@ -156,7 +156,7 @@ def contract(a: Tensor, b: Tensor) -> Tensor:
     return _finish(_panel(a2, b2, 0, k, b_mult), b_mult, ol, od)
 
 
-# -- reference contract.py:168-208 ------------------------------------------------
+# -- reference contract.py:168-208 (split_common_contract) --
 def split_common(a: Tensor, b: Tensor, blocks: int, group: int) -> Tensor:
     a2, b2, (m, k, n), b_mult, ol, od = _operands(a, b)
     panels = min(blocks * group, k)
@@ -168,7 +168,7 @@ def split_common(a: Tensor, b: Tensor, blocks: int, group: int) -> Tensor:
     return _finish(parts[0], b_mult, ol, od)
 
 
-# -- reference execute.py:345-386 (step loop, "single" = c64 at rest, c128 in flight)
+# -- reference execute.py:119-178 (_Engine.fetch / run_range step loop, "single" = c64 at rest, c128 in flight)
 def run_range(leaves: Sequence[Tensor], steps, n_leaves: int, lo: int, hi: int,
               assignment: dict[str, int], values: dict, precision: str = "single") -> dict:
     """steps: sequence of (lhs, rhs, result) SSA triples (1-based lo..hi inclusive)."""
@@ -196,7 +196,7 @@ def cast_leaves(leaves: Sequence[Tensor], precision: str = "single") -> list[Ten
     return [(l, d, np.asarray(x).astype(dt)) for l, d, x in leaves]
 
 
-# -- reference execute.py:412-438 ---------------------------------------------------
+# -- reference execute.py:115-116, 204-230 (_enumerate, run_sliced) --
 def run_sliced(leaves, steps, n_leaves: int, slice_labels: Sequence[str], slice_dims: Sequence[int],
                precision: str = "single", keys: Sequence[tuple] | None = None):
     """Sum over slice assignments (itertools.product order) of full runs.
@@ -213,7 +213,7 @@ def run_sliced(leaves, steps, n_leaves: int, slice_labels: Sequence[str], slice_
     return acc, partials
 
 
-# -- reference execute.py:305-320 ---------------------------------------------------
+# -- reference execute.py:97-112 (hierarchical_reduce) --
 def hierarchical_reduce(vals: Sequence, group_size: int = 256):
     groups = []
     for lo in range(0, len(vals), group_size):
@@ -227,7 +227,7 @@ def hierarchical_reduce(vals: Sequence, group_size: int = 256):
     return total
 
 
-# -- reference execute.py:441-521 (spindle program interpreter) ---------------------
+# -- reference execute.py:233-313 (_run_program: spindle program interpreter) --
 def run_program(leaves, steps, n_leaves: int, actions, outer_assignment: dict[str, int],
                 dep_sets: dict[str, set], precision: str = "single"):
     """actions: list of dicts in the reference's ReuseAction.to_obj() format."""
@@ -277,7 +277,7 @@ def run_program(leaves, steps, n_leaves: int, actions, outer_assignment: dict[st
     return acc
 
 
-# -- complex128 state vector (independent amplitude check, oracles.py:76-104) -------
+# -- complex128 state vector (independent amplitude check, tests/oracles.py:76-104) --
 def statevector(n_qubits: int, gates) -> np.ndarray:
     """Vectorised complex128 state vector; qubit q occupies bit q.
     ``gates``: iterable of (qubits tuple, unitary matrix)."""

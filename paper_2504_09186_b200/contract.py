@@ -4,10 +4,17 @@ API mirror of ``tncsim.contract`` (``contract.py:1-208``): ``contract_pair``,
 ``split_common_contract``, ``contraction_shape``, ``multiply_cost``,
 ``ttgt_plan``, ``contraction_permutations``.  The index map is the
 reference's (result legs free_A ++ free_B, ``contract.py:149-165``); the
-arithmetic runs in the sm_100a kernels selected by ``tnc_plan_contract``:
-3xTF32 tcgen05 GEMM for tensor-core-sized steps, CUDA-core GEMM otherwise,
-split-K with the reference's panel/tree semantics for
-``split_common_contract``.
+arithmetic runs in the sm_100a kernels selected by ``tnc_plan_contract``
+(AUTO):
+
+* K2: tcgen05 ``kind::f16`` GEMM on 3xFP16 operand planes (per-row
+  power-of-two scaling) for big tensor-core-shaped steps;
+* K6: gather-fed tcgen05 ``kind::tf32`` GEMM (3xTF32, operands gathered in the
+  kernel, split-K) for narrow / split-K-shaped steps;
+* K5 streaming and K3 split-K kernels for the narrowest steps, the CUDA-core
+  GEMM for small ones;
+* split-K with the reference's panel/tree semantics for
+  ``split_common_contract``.
 """
 
 from __future__ import annotations
@@ -87,7 +94,9 @@ def _dtype_code(t: torch.Tensor) -> int:
 def plan_for(a_indices, a_strides, b_indices, b_strides, dtype: int,
              out_order: Sequence[Index] | None = None, variant: int = _lib.VARIANT_AUTO) -> ContractPlan:
     """Cached device plan for contracting two labeled strided operands."""
+    # plans own lazily-created device tables: one plan per device
     key = (
+        torch.cuda.current_device() if torch.cuda.is_available() else -1,
         tuple((ix.label, ix.dim) for ix in a_indices), tuple(a_strides),
         tuple((ix.label, ix.dim) for ix in b_indices), tuple(b_strides), dtype,
         None if out_order is None else tuple(ix.label for ix in out_order), variant,

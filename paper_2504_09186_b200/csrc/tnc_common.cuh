@@ -51,6 +51,23 @@ void count_launch();
     if (_s != TNC_OK) return _s; \
   } while (0)
 
+// 3xFP16 per-row scale exponent: the row is multiplied by 2^-e so that its
+// largest |component| lands in [2^14, 2^15).  Scaling to the top of the fp16
+// range (rather than to [0.5, 1)) keeps the lo = fp16(x - hi) plane normal
+// down to 2^-16 of the row maximum and its subnormal step at 2^-38 of it, so
+// rows with a large max/rms ratio keep fp32-class accuracy.  e is clamped so
+// that 2^-e stays a normal float.
+constexpr int kF16ScaleBits = 15;
+__host__ __device__ __forceinline__ int f16_row_exponent(float mx) {
+  int e = 0;
+  if (mx > 0.f && isfinite(mx)) {
+    frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+    e -= kF16ScaleBits;
+    if (e < -126) e = -126;
+  }
+  return e;
+}
+
 // complex element types (interleaved re, im), 8 and 16 bytes
 struct __align__(8) c64 {
   float re, im;

@@ -435,9 +435,10 @@ __global__ void tf32_split_kernel(int mode, int64_t R, int64_t K, int64_t Kp,
 }
 
 // 2-piece FP16 operand planes with a power-of-two scale per row ("3xFP16"):
-//   row r is scaled by 2^-e[r] so its largest |component| lies in [0.5, 1),
-//   hi = fp16(x), lo = fp16(x - hi); then x = 2^e (hi + lo) to ~2^-25 of the
-//   row maximum (fp16 subnormals cover the tail), and
+//   row r is scaled by 2^-e[r] so its largest |component| lies in
+//   [2^14, 2^15) (f16_row_exponent), hi = fp16(x), lo = fp16(x - hi); then
+//   x = 2^e (hi + lo) to ~2^-22 relative down to 2^-16 of the row maximum and
+//   to ~2^-38 of the row maximum below that (fp16 subnormals), and
 //   x*y ~= hi*hi' + hi*lo' + lo*hi' keeps fp32-class accuracy relative to the
 //   row/column norms with half the operand bytes of 3xTF32 and the 2x-rate
 //   kind::f16 tensor-core path.  One warp per row.
@@ -458,8 +459,7 @@ __global__ void __launch_bounds__(256) f16_split_kernel(int mode, int64_t R, int
     }
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
-    int e = 0;
-    if (mx > 0.f && isfinite(mx)) frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+    const int e = f16_row_exponent(mx);
     if (lane == 0) exps[r] = e;
     const float sc = ldexpf(1.f, -e);
     for (int64_t k = lane; k < Kp; k += 32) {
@@ -515,8 +515,7 @@ __global__ void f16_split_elem_kernel(int mode, int64_t R, int64_t K, int64_t Kp
     const int64_t r = e / Kp;
     const int64_t k = e - r * Kp;
     const float mx = __uint_as_float(rowmax[r]);
-    int ex = 0;
-    if (mx > 0.f && isfinite(mx)) frexpf(mx, &ex);
+    const int ex = f16_row_exponent(mx);
     if (k == 0) exps[r] = ex;
     const float sc = ldexpf(1.f, -ex);
     float re = 0.f, im = 0.f;

@@ -1,11 +1,16 @@
-// K2: complex GEMM on 5th-gen tensor cores, 3xTF32 split, TMEM accumulate.
+// K2: complex GEMM on 5th-gen tensor cores, 3-product split, TMEM accumulate.
 //
 // Reference op: the np.matmul inside contract_pair (contract.py:131-165),
 // which the reference runs in complex128 for "single" tensors
-// (execute.py:154-158).  fp32 accuracy is kept with the 3xTF32 scheme
-//     x*y ~= big(x)*big(y) + big(x)*small(y) + small(x)*big(y)
-// (big = nearest TF32, small = x - big), all three products issued as
-// tcgen05.mma kind::tf32 into one fp32 TMEM accumulator.
+// (execute.py:154-158).  fp32 accuracy is kept with a 3-product split
+//     x*y ~= hi(x)*hi(y) + hi(x)*lo(y) + lo(x)*hi(y)
+// issued as three tcgen05.mma into one fp32 TMEM accumulator.  Two operand
+// formats (template flag F16):
+//   * 3xFP16 (AUTO default): hi = fp16(x * 2^-e), lo = fp16(x * 2^-e - hi)
+//     with a per-row power-of-two scale (f16_row_exponent), kind::f16;
+//     the epilogue multiplies by 2^(e_row + e_col);
+//   * 3xTF32 (TNC_TC_TF32=1, and K <= 16): big = nearest TF32, small =
+//     x - big, kind::tf32.
 //
 // Complex arithmetic is folded into ONE real GEMM:
 //     A  (complex [M, K], interleaved)      == real [M, 2K]
@@ -175,12 +180,6 @@ struct TcParams {
   const int* ey;         // 3xFP16: per-complex-column scale exponent of B
 };
 
-// 2^e as a float: exponent-field construction on the normal range, ldexpf
-// for the (rare) subnormal results
-__device__ __forceinline__ float pow2i(int e) {
-  return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.f, e);
-}
-
 // Undo the 3xFP16 per-row / per-column power-of-two operand scaling of one
 // thread's row segment (HALF fp32 = HALF/2 complex columns from ncol0).  The
 // column exponents come in as 16-byte vectors (ncol0 is a multiple of 4 and
@@ -199,15 +198,18 @@ __device__ __forceinline__ void unscale(float (&acc)[HALF], const TcParams& p, i
       if (ncol0 + 4 * q + 1 < p.N) e.y = p.ey[ncol0 + 4 * q + 1];
       if (ncol0 + 4 * q + 2 < p.N) e.z = p.ey[ncol0 + 4 * q + 2];
     }
-    const float s0 = pow2i(er + e.x), s1 = pow2i(er + e.y), s2 = pow2i(er + e.z), s3 = pow2i(er + e.w);
-    acc[8 * q + 0] *= s0;
-    acc[8 * q + 1] *= s0;
-    acc[8 * q + 2] *= s1;
-    acc[8 * q + 3] *= s1;
-    acc[8 * q + 4] *= s2;
-    acc[8 * q + 5] *= s2;
-    acc[8 * q + 6] *= s3;
-    acc[8 * q + 7] *= s3;
+    const int es[4] = {er + e.x, er + e.y, er + e.z, er + e.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (es[j] >= -126 && es[j] <= 127) {
+        const float sc = __int_as_float((es[j] + 127) << 23);
+        acc[8 * q + 2 * j] *= sc;
+        acc[8 * q + 2 * j + 1] *= sc;
+      } else {  // combined scale outside the normal range: exact ldexp on the value
+        acc[8 * q + 2 * j] = ldexpf(acc[8 * q + 2 * j], es[j]);
+        acc[8 * q + 2 * j + 1] = ldexpf(acc[8 * q + 2 * j + 1], es[j]);
+      }
+    }
   }
 }
 

@@ -405,8 +405,7 @@ __global__ void rowmax_to_exp_kernel(int64_t R, unsigned* __restrict__ rowmax, i
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < R;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float mx = __uint_as_float(rowmax[r]);
-    int e = 0;
-    if (mx > 0.f && isfinite(mx)) frexpf(mx, &e);  // same rule as f16_split_kernel
+    const int e = f16_row_exponent(mx);  // same rule as f16_split_kernel
     exps[r] = e;
     rowmax[r] = __float_as_uint(ldexpf(1.f, -e));
   }

@@ -205,21 +205,22 @@ class Engine:
         return DenseTensor.__new__(DenseTensor)._init_raw(plan.out_indices, contract_into(plan, lhs.data, rhs.data))
 
     def run_range(self, s: LinearSchedule, lo: int, hi: int, assignment: dict[str, int], values: dict,
-                  stats: RunStats, aux_bytes: int = 0, cache: dict | None = None) -> None:
+                  stats: RunStats, aux_bytes: int = 0, cache: dict | None = None,
+                  invariant: set | frozenset = frozenset()) -> None:
         """Steps lo..hi (1-based, inclusive) -- reference ``execute.py:137-178``.
-        ``cache`` (slice-invariant step results, see ``ReuseRunner``) short-cuts
-        steps whose result no sliced label reaches."""
+
+        ``invariant`` (results no sliced label reaches, see ``ReuseRunner``)
+        are never recomputed: a result some dependent step consumes is taken
+        from ``cache``; the others only feed further invariant steps and are
+        skipped."""
         rate = self.rate
         live = sum(v.size for v in values.values())
         for pos in range(lo - 1, hi):
             step = s.steps[pos]
-            if cache is not None and step.result in cache:
-                for ref in (step.lhs, step.rhs):
-                    if ref >= s.n_leaves and ref in values:
-                        live -= values[ref].size
-                        del values[ref]
-                values[step.result] = cache[step.result]
-                live += values[step.result].size
+            if step.result in invariant:
+                if step.result in cache:
+                    values[step.result] = cache[step.result]
+                    live += values[step.result].size
                 continue
             lhs = self.fetch(s, step.lhs, assignment, values)
             rhs = self.fetch(s, step.rhs, assignment, values)
@@ -309,7 +310,8 @@ def _add(a: DenseTensor, b: DenseTensor) -> DenseTensor:
 
 
 def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets: dict[str, set[int]],
-                 mem_budget: int | None, open_root: bool = False, cache: dict | None = None):
+                 mem_budget: int | None, open_root: bool = False, cache: dict | None = None,
+                 invariant: set | frozenset = frozenset()):
     """Device interpreter of a reuse action program (reference
     ``execute.py:233-313``).  Tensors are immutable, so CHECKPOINT / STORE
     keep references; MERGE sums the dependent values with the axpy kernel.
@@ -347,7 +349,7 @@ def _run_program(eng: Engine, rs: ReuseSchedule, outer: dict[str, int], dep_sets
         if act.kind == RUN:
             asn = dict(outer)
             asn.update(dict(act.assignment))
-            eng.run_range(s, act.lo, act.hi, asn, values, stats, aux_bytes(), cache)
+            eng.run_range(s, act.lo, act.hi, asn, values, stats, aux_bytes(), cache, invariant)
             parked = False
         elif act.kind == CHECKPOINT:
             snap = dict(values)
@@ -464,6 +466,13 @@ class ReuseRunner:
         for label in labels:
             dep |= dependent_results(self.s, label)
         self.invariant_positions = [p for p, st in enumerate(self.s.steps) if st.result not in dep]
+        self.invariant = frozenset(self.s.steps[p].result for p in self.invariant_positions)
+        # invariant results a dependent step (or the root) consumes: the cache
+        self.needed = set()
+        for st in self.s.steps:
+            if st.result in dep:
+                self.needed.update(r for r in (st.lhs, st.rhs) if r in self.invariant)
+        self.needed.add(self.s.steps[-1].result)
         self.deps = {e.index.label: dependent_results(self.s, e.index.label) for e in rs.nested}
         self.outer_labels = tuple(e.index.label for e in rs.outer)
         self.outer_dims = tuple(e.index.dim for e in rs.outer)
@@ -473,10 +482,21 @@ class ReuseRunner:
         self.stats = RunStats()
 
     def prepare(self) -> None:
+        """Evaluate every slice-invariant step once; keep the results that a
+        dependent step consumes (the programs never recompute invariant
+        steps: ``Engine.run_range(..., invariant=...)``)."""
         values: dict = {}
+        eng, s = self.eng, self.s
         for p in self.invariant_positions:
-            self.eng.run_range(self.s, p + 1, p + 1, {}, values, self.stats)
-        self.cache = values
+            st = s.steps[p]
+            lhs, rhs = eng.fetch(s, st.lhs, {}, values), eng.fetch(s, st.rhs, {}, values)
+            out = eng.contract(lhs, rhs)
+            self.stats.multiplies += multiply_cost(lhs.indices, rhs.indices)
+            for ref in (st.lhs, st.rhs):
+                if ref >= s.n_leaves and ref not in self.needed:
+                    values.pop(ref, None)
+            values[st.result] = out
+        self.cache = {k: v for k, v in values.items() if k in self.needed}
 
     def outer_assignment(self, program_id: int) -> dict[str, int]:
         """Mixed radix over the outer labels, first label most significant."""
@@ -490,7 +510,7 @@ class ReuseRunner:
         if self.cache is None:
             self.prepare()
         root, st = _run_program(self.eng, self.rs, self.outer_assignment(program_id), self.deps,
-                                self.mem_budget, open_root=True, cache=self.cache)
+                                self.mem_budget, open_root=True, cache=self.cache, invariant=self.invariant)
         self.stats.multiplies += st.multiplies
         self.stats.subtasks_done += self.slices_per_program
         return root

@@ -1,0 +1,299 @@
+"""Full-size parity through an independent complex128 device checker and
+sampled sub-slices the CPU oracle can finish (BASELINE configs C2, C3, C4).
+
+Chain of evidence:
+
+1. ``devcheck`` (plain torch complex128 gathers + zgemm, reference
+   semantics) is pinned to the reference's own outputs: the C0 open root the
+   reference computed and the 4x4 fixture's per-slice roots.
+2. The engine matches the checker on the FULL cap-30 C3 slice the bench
+   times, on the rank-30 C2 chain, and on cap-30 sub-slices of C4 slices.
+3. The engine matches the numpy oracle of the reference step loop on cap-26
+   sub-slices of the first 4 timed C4 slices (north star: "checked against
+   the reference oracle on the first 4 slices").
+4. A cap-32 C4 slice equals the sum of its two sub-slices under one more
+   sliced label (linearity of the slice sum, reference ``execute.py:204-230``).
+5. The 3xFP16 operand split keeps rel-L2 <= 1e-5 on adversarial rows whose
+   bulk sits 10^3..10^6 below a spike the other operand annihilates.
+"""
+
+import gc
+
+import numpy as np
+import pytest
+import torch
+
+import devcheck
+from conftest import arr, load_golden, rel_l2
+from oracle import tncref
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # north star: rel-L2 <= 1e-5 for complex64 amplitudes
+
+
+def _free():
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def _rel(got: torch.Tensor, want: torch.Tensor) -> float:
+    got = got.reshape(-1).to(torch.complex128)
+    want = want.reshape(-1).to(torch.complex128)
+    return ((got - want).norm() / want.norm()).item()
+
+
+def _leaves(net):
+    """Leaves rounded to complex64 as the reference "single" engine does
+    (execute.py:128), held as complex128 on the device."""
+    host = tncref.cast_leaves([(t.labels, t.dims, t.numpy()) for t in net.tensors], "single")
+    return devcheck.to_device(host)
+
+
+def _steps(s):
+    return [(st.lhs, st.rhs, st.result) for st in s.steps]
+
+
+def _by_labels(t, labels):
+    from paper_2504_09186_b200 import permute
+
+    by = {ix.label: ix for ix in t.indices}
+    return permute(t, [by[l] for l in labels])
+
+
+# -- 1. the checker is pinned to the reference ------------------------------------
+
+
+def test_checker_matches_reference_c0_open_root(cuda_ready):
+    from paper_2504_09186_b200 import circuit_to_network, greedy_path, linearize, parse_circuit
+
+    g = load_golden("c0")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits, open_qubits=g["open"]["qubits"])
+    s = linearize(greedy_path(net, 0))
+    root = devcheck.run_schedule(_leaves(net), _steps(s), s.n_leaves, {})
+    assert list(root[0]) == g["open"]["root_labels"]
+    # reference single mode: c64 leaves, c128 in flight, c64 at the end
+    assert rel_l2(root[2].cpu().numpy(), arr(g["open"]["root_single"])) <= 1e-6
+    assert rel_l2(root[2].cpu().numpy().astype(np.complex64), arr(g["open"]["root_single"])) <= 1e-7
+
+
+def test_checker_matches_reference_per_slice_roots(cuda_ready):
+    import json
+
+    from paper_2504_09186_b200 import SliceSpec, circuit_to_network, greedy_path, linearize, parse_circuit
+
+    g = load_golden("sliced")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits, open_qubits=g["open"])
+    s = linearize(greedy_path(net, 0))
+    spec = SliceSpec.from_json(json.dumps(g["open_net"]["slice_spec"]))
+    leaves = _leaves(net)
+    for sid in (0, 1, 7, 63, len(g["open_net"]["per_slice"]) - 1):
+        item = g["open_net"]["per_slice"][sid]
+        root = devcheck.run_schedule(leaves, _steps(s), s.n_leaves, spec.assignment(sid))
+        got = devcheck.permute(root, item["labels"])[2].cpu().numpy()
+        assert rel_l2(got, arr(item["data"])) <= 1e-6
+
+
+# -- 2. engine vs checker at full size ---------------------------------------------
+
+
+def _plan(name):
+    from paper_2504_09186_b200 import greedy_path, linearize, select_slices, workloads
+
+    wl, cap = (workloads.C3, workloads.C3_MAX_RANK) if name == "c3" else (workloads.C4, workloads.C4_MAX_RANK)
+    net = wl.network()
+    t = greedy_path(net, 0)
+    return wl, net, t, linearize(t), select_slices(t, cap, 64, 0)
+
+
+def _c4_timed_ids(spec, n=4):
+    """The bench's seeded 2^10 subset of C4 slice ids (bench.plan_workload)."""
+    ids = sorted(int(x) for x in np.random.default_rng(0).choice(spec.n_subtasks, 1024, replace=False))
+    return ids[:n]
+
+
+def test_c3_full_slice_vs_checker(cuda_ready):
+    """The cap-30 C3 slice the bench times (slice 0), all 779 steps, vs the
+    complex128 checker; labels identical (the reference index map)."""
+    from paper_2504_09186_b200.execute import SliceExecutor
+
+    wl, net, t, s, spec = _plan("c3")
+    asn = spec.assignment(0)
+    ex = SliceExecutor(net, s, spec, "single")
+    got = ex.run_slice(asn)
+    got_labels, got_data = list(got.labels), got.data.clone()
+    del ex, got
+    _free()
+    root = devcheck.run_schedule(_leaves(net), _steps(s), s.n_leaves, asn)
+    assert got_labels == list(root[0])
+    err = _rel(got_data, root[2])
+    del root
+    _free()
+    assert err <= TOL, err
+
+
+def test_c2_chain_vs_checker(cuda_ready):
+    """Rank-30 tensor (8 GiB) absorbing the 16 C2 gates: fused K4 chain vs the
+    complex128 checker's 16 contract_pair(T, G) steps."""
+    from paper_2504_09186_b200 import DenseTensor, Index
+    from paper_2504_09186_b200.fusion import absorb_chain
+    from paper_2504_09186_b200.workloads import C2
+
+    t_labels, data, gates = C2.build()
+    t = DenseTensor([Index(l) for l in t_labels], data)
+    gs = [DenseTensor([Index(oa), Index(ob), Index(ia), Index(ib)], u) for ia, ib, oa, ob, u in gates]
+    fused = absorb_chain(t, gs)
+    fused_labels = list(fused.labels)
+    del t
+    _free()
+    cur = (tuple(t_labels), (2,) * len(t_labels),
+           torch.from_numpy(data).cuda().to(torch.complex128))
+    del data
+    for ia, ib, oa, ob, u in gates:
+        g = ((oa, ob, ia, ib), (2, 2, 2, 2), torch.from_numpy(u).cuda().to(torch.complex128))
+        cur = devcheck.contract(cur, g)
+    assert fused_labels == list(cur[0])
+    err = _rel(fused.data, cur[2])
+    del cur, fused
+    _free()
+    assert err <= TOL, err
+
+
+def test_c4_cap30_subslices_vs_checker(cuda_ready):
+    """Two cap-30 sub-slices (replay-style extra slicing, 5 more labels) of the
+    first timed C4 slice vs the complex128 checker."""
+    from paper_2504_09186_b200 import select_slices
+    from paper_2504_09186_b200.execute import SliceExecutor
+
+    wl, net, t, s, spec = _plan("c4")
+    sub = select_slices(t, 30, 64, 0)
+    assert sub.labels[: len(spec.labels)] == spec.labels  # refinement of the cap-32 slicing
+    extra = sub.n_subtasks // spec.n_subtasks
+    sid0 = _c4_timed_ids(spec, 1)[0]
+    ex = SliceExecutor(net, s, sub, "single")
+    got = {}
+    for v in (0, extra - 1):
+        r = ex.run_slice(sub.assignment(sid0 * extra + v))
+        got[v] = (list(r.labels), r.data.clone())
+    del ex, r
+    _free()
+    leaves = _leaves(net)
+    for v, (labels, data) in got.items():
+        root = devcheck.run_schedule(leaves, _steps(s), s.n_leaves, sub.assignment(sid0 * extra + v))
+        assert labels == list(root[0])
+        err = _rel(data, root[2])
+        del root
+        _free()
+        assert err <= TOL, (v, err)
+
+
+# -- 3. engine vs the numpy oracle on the first 4 timed C4 slices -------------------
+
+
+def test_c4_first_four_slices_subslices_vs_oracle(cuda_ready):
+    """Cap-26 sub-slices (18 more sliced labels) of the first 4 timed C4
+    slices: the engine vs the numpy oracle of the reference step loop."""
+    from paper_2504_09186_b200 import select_slices
+    from paper_2504_09186_b200.execute import SliceExecutor
+
+    wl, net, t, s, spec = _plan("c4")
+    sub = select_slices(t, 26, 64, 0)
+    assert sub.labels[: len(spec.labels)] == spec.labels
+    extra = sub.n_subtasks // spec.n_subtasks
+    ex = SliceExecutor(net, s, sub, "single")
+    leaves = tncref.cast_leaves([(tt.labels, tt.dims, tt.numpy()) for tt in net.tensors], "single")
+    rng = np.random.default_rng(4)
+    for sid in _c4_timed_ids(spec, 4):
+        asn = sub.assignment(sid * extra + int(rng.integers(extra)))
+        got = ex.run_slice(asn)
+        vals = tncref.run_range(leaves, _steps(s), s.n_leaves, 1, len(s.steps), asn, {}, "single")
+        ref = vals[s.steps[-1].result]
+        assert list(got.labels) == list(ref[0])
+        assert rel_l2(got.numpy(), ref[2]) <= TOL
+
+
+# -- 4. slice-sum linearity at the C4 cap ---------------------------------------------
+
+
+def test_c4_slice_equals_sum_of_two_subslices(cuda_ready):
+    from paper_2504_09186_b200 import SliceSpec, select_slices
+    from paper_2504_09186_b200.execute import SliceExecutor
+
+    wl, net, t, s, spec = _plan("c4")
+    sid = _c4_timed_ids(spec, 1)[0]
+    ex = SliceExecutor(net, s, spec, "single")
+    whole = ex.run_slice(spec.assignment(sid))
+    whole_labels, whole_data = list(whole.labels), whole.data.to(torch.complex128)
+    del ex, whole
+    _free()
+    finer = select_slices(t, 31, 64, 0)
+    spec2 = SliceSpec(list(finer.entries[: len(spec.entries) + 1]))
+    assert spec2.labels[:-1] == spec.labels
+    ex2 = SliceExecutor(net, s, spec2, "single")
+    d = spec2.dims[-1]
+    total = None
+    for v in range(d):
+        part = ex2.run_slice(spec2.assignment(sid * d + v))
+        assert list(part.labels) == whole_labels
+        total = part.data.to(torch.complex128) if total is None else total + part.data.to(torch.complex128)
+    del ex2, part
+    _free()
+    assert _rel(total, whole_data) <= TOL
+
+
+# -- 5. 3xFP16 dynamic-range stress -------------------------------------------------
+
+
+def _spiky_pair(m_bits, k_bits, n_bits, spike, seed, shuffle):
+    """A[m, k], B[k, n] Gaussian; A has a spike of `spike` x the bulk in column
+    k0 of every row and B row k0 is zero (and vice versa for k1 / B): the
+    spikes set the per-row scale but contribute nothing to C."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    m, k, n = 1 << m_bits, 1 << k_bits, 1 << n_bits
+    a = torch.randn(m, k, dtype=torch.complex64, device="cuda", generator=g)
+    b = torch.randn(k, n, dtype=torch.complex64, device="cuda", generator=g)
+    a[:, 3] = spike * (1 + 1j)
+    b[3, :] = 0
+    b[5, :] = spike * (1 - 1j)
+    a[:, 5] = 0
+    la = [f"a{i}" for i in range(m_bits)] + [f"k{i}" for i in range(k_bits)]
+    lb = [f"k{i}" for i in range(k_bits)] + [f"b{i}" for i in range(n_bits)]
+    want = (a.to(torch.complex128) @ b.to(torch.complex128)).reshape(-1)
+    a_data, b_data = a.reshape(-1), b.reshape(-1)
+    if shuffle:  # permuted operands: exercises the fused gather + split path
+        rng = np.random.default_rng(seed)
+        pa, pb = rng.permutation(len(la)), rng.permutation(len(lb))
+        a_data = a.reshape((2,) * len(la)).permute(*pa.tolist()).contiguous().reshape(-1)
+        b_data = b.reshape((2,) * len(lb)).permute(*pb.tolist()).contiguous().reshape(-1)
+        la, lb = [la[i] for i in pa], [lb[i] for i in pb]
+    out = [f"a{i}" for i in range(m_bits)] + [f"b{i}" for i in range(n_bits)]
+    return la, a_data, lb, b_data, out, want
+
+
+@pytest.mark.parametrize("spike", [1e3, 1e4, 1e5, 1e6])
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_f16_split_dynamic_range(cuda_ready, spike, shuffle):
+    from paper_2504_09186_b200 import DenseTensor, Index, _lib, contract_pair
+
+    la, ad, lb, bd, out, want = _spiky_pair(9, 12, 9, spike, 7, shuffle)
+    got = contract_pair(DenseTensor([Index(l) for l in la], ad), DenseTensor([Index(l) for l in lb], bd),
+                        out_order=[Index(l) for l in out], variant=_lib.VARIANT_TC3XF16)
+    assert _rel(got.data, want) <= TOL
+
+
+@pytest.mark.parametrize("spike", [1e4, 1e6])
+def test_auto_dynamic_range_on_k2_shape(cuda_ready, spike):
+    """AUTO on a K2-shaped step (rows_x > 128 * SMs): the plan picks the 3xFP16
+    kernel and stays within the tolerance on spiky rows."""
+    from paper_2504_09186_b200 import DenseTensor, Index, _lib
+    from paper_2504_09186_b200.contract import contract_into, plan_for
+
+    la, ad, lb, bd, out, want = _spiky_pair(15, 11, 8, spike, 8, True)
+    ia, ib = [Index(l) for l in la], [Index(l) for l in lb]
+    plan = plan_for(ia, ad.stride(), ib, bd.stride(), _lib.C64, [Index(l) for l in out])
+    assert plan.variant == _lib.VARIANT_TC3XF16
+    got = contract_into(plan, ad, bd)
+    assert _rel(got, want) <= TOL

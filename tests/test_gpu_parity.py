@@ -359,11 +359,22 @@ def test_open_output_spindle_reuse(cuda_ready):
     from paper_2504_09186_b200.execute import ReuseRunner
 
     part = choose_reuse_subset(t, spec, None, 3)
-    rs, _ = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    rs, rep3 = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
     rr = ReuseRunner(net, rs, "single", labels0)
     assert rr.n_programs * rr.slices_per_program == spec.n_subtasks
     got = rr.finish(rr.run(range(rr.n_programs))).numpy()
     assert rel_l2(got, want) <= TOL_C64
+    # invariant steps run once (prepare), never inside a program: executed
+    # multiplies = invariant work + per program the dependent steps of its RUNs
+    from paper_2504_09186_b200.execute import _proj_cost
+    from paper_2504_09186_b200.reuse import RUN
+
+    dims = {e.index.label: 1 for e in list(rs.outer) + list(rs.nested)}
+    inv = sum(_proj_cost(rs.schedule, p, dims) for p in rr.invariant_positions)
+    per_program = sum(_proj_cost(rs.schedule, p, dims) for a in rs.actions if a.kind == RUN
+                      for p in range(a.lo - 1, a.hi) if rs.schedule.steps[p].result not in rr.invariant)
+    assert rr.stats.multiplies == inv + rr.n_programs * per_program
+    assert rr.stats.multiplies <= rep3.predicted_multiplies
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
