@@ -47,6 +47,48 @@ def _dist_env():
     return world, rank, local
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(argv: list[str], n: int) -> int:
+    """Re-exec this script under torch.distributed.run with one rank per GPU
+    (when ``--gpus N`` is given without a torchrun environment)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *argv]
+    env = dict(os.environ)
+    # communicator setup lines (rank count, NVLS / NVLink transports) on stderr;
+    # stdout carries only rank 0's JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.call(cmd, env=env)
+
+
+def init_dist(backend: str, local: int):
+    """Process group over torchrun's env (MASTER_ADDR / PORT, RANK, WORLD_SIZE)."""
+    import torch
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
+def step_unit_ids(unit_ids: list[int], step: int, world: int, per_rank: int) -> list[int]:
+    """The job-wide unit ids of one step: world * per_rank consecutive entries
+    of the (cyclic) id list; ``distributed.partition`` deals them round-robin."""
+    n = len(unit_ids)
+    base = step * world * per_rank
+    return [unit_ids[(base + j) % n] for j in range(world * per_rank)]
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
 
@@ -232,10 +274,12 @@ def bench_c3(args) -> None:
     from paper_2504_09186_b200 import _lib
     from paper_2504_09186_b200.execute import SliceExecutor, run_open
 
+    from paper_2504_09186_b200.distributed import accumulate_rank_units, allreduce_partial
+
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist("nccl", local)
     lib = _lib.load(require_device=True)
     wl, net, t, s, spec, per_slice, slice_ids = plan_workload(args.workload)
     order = wl.output_order()
@@ -267,13 +311,9 @@ def bench_c3(args) -> None:
     n_ids = len(slice_ids)
     spp = args.slices_per_step
 
-    def ids_for(step: int):
-        base = (step * world + rank) * spp
-        return [slice_ids[(base + j) % n_ids] for j in range(spp)]
-
     acc = None
     for i in range(args.warmup):
-        acc = ex.run(ids_for(i), acc)
+        acc = accumulate_rank_units(ex, step_unit_ids(slice_ids, i, world, spp), world, rank, acc)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -289,9 +329,9 @@ def bench_c3(args) -> None:
     start.record(stream)
     part = None
     for i in range(args.steps):
-        part = ex.run(ids_for(args.warmup + i), part)
+        part = accumulate_rank_units(ex, step_unit_ids(slice_ids, args.warmup + i, world, spp), world, rank, part)
     if world > 1:
-        dist.all_reduce(part.data.view(torch.float32), op=dist.ReduceOp.SUM)
+        allreduce_partial(part.data)  # the one collective: NCCL all-reduce of the partial amplitudes
     stop.record(stream)
     torch.cuda.synchronize()
     launches = lib.tnc_launch_count() - launches0
@@ -382,7 +422,10 @@ def bench_c3(args) -> None:
                        "spindle_reuse": reuse_info,
                        "executed_tflops": (8 * executed_mult / elapsed / 1e12) if reuse_info else None,
                        "flops_per_slice": 8 * per_slice, "l2": "inputs > L2 (intermediates up to 8 GiB)",
-                       "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce"},
+                       "parallelism": f"slices round-robin over {world} GPU(s) + 1 NCCL all-reduce",
+                       "nccl": ({"world": dist.get_world_size(), "backend": dist.get_backend(),
+                                 "version": ".".join(map(str, torch.cuda.nccl.version()))}
+                                if world > 1 else None)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_eff, "unit": "TFLOP/s",
                          "frac": (achieved / p_eff) if achieved else None,
@@ -397,6 +440,67 @@ def bench_c3(args) -> None:
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.destroy_process_group()
+
+
+class _DryExecutor:
+    """Kernel-free stand-in for the slice executor (``--dry-run``): slice i's
+    root is a known complex vector, so the launcher, the round-robin deal and
+    the all-reduce can be checked on CPU ranks (gloo)."""
+
+    n_roots = 64
+
+    def __init__(self, n_units: int):
+        import torch
+
+        self.n_units = n_units
+        self.seen: list[int] = []
+        self._t = torch
+
+    def root(self, sid: int):
+        t = self._t
+        k = t.arange(self.n_roots, dtype=t.float64)
+        return t.complex(t.cos(0.1 * sid * k), t.sin(0.3 * sid + k))
+
+    def run(self, ids, acc=None):
+        for sid in ids:
+            self.seen.append(sid)
+            r = self.root(sid)
+            acc = r.clone() if acc is None else acc + r
+        return acc
+
+    def zeros(self):
+        return self._t.zeros(self.n_roots, dtype=self._t.complex128)
+
+
+def bench_dry(args) -> None:
+    """--dry-run: the multi-rank bench loop without kernels (gloo on CPU)."""
+    import torch
+
+    from paper_2504_09186_b200.distributed import accumulate_rank_units, allreduce_partial
+
+    world, rank, local = _dist_env()
+    dist = init_dist("gloo", local) if world > 1 else None
+    ex = _DryExecutor(512)
+    ids = list(range(ex.n_units))
+    acc = None
+    steps = args.warmup + args.steps
+    for i in range(steps):
+        acc = accumulate_rank_units(ex, step_unit_ids(ids, i, world, args.slices_per_step), world, rank, acc)
+    if world > 1:
+        allreduce_partial(acc)
+        seen = [None] * world
+        dist.all_gather_object(seen, ex.seen)
+    else:
+        seen = [ex.seen]
+    want = None
+    for i in range(steps):
+        want = ex.run(step_unit_ids(ids, i, world, args.slices_per_step), want)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "per_rank_ids": seen, "max_abs_err": float((acc - want).abs().max()),
+                          "backend": dist.get_backend() if dist else None}), flush=True)
+    if dist:
         dist.destroy_process_group()
 
 
@@ -548,10 +652,20 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reuse", type=int, default=0,
                     help="spindle reuse with this many nested sliced labels (0: slice-invariant reuse only)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="kernel-free multi-rank loop on CPU (gloo): launcher / deal / all-reduce check")
     args = ap.parse_args()
     import paper_2504_09186_b200._lib as _l  # noqa: F401  (fail fast if the package is broken)
     if args.impl == "reference":
         bench_reference(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(sys.argv[1:], args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if args.dry_run:
+        bench_dry(args)
         return
     {"c3": bench_c3, "c4": bench_c3, "c2": bench_c2, "c1": bench_c1}[args.workload](args)
 

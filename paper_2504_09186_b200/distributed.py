@@ -51,33 +51,53 @@ def allreduce_partial(partial: torch.Tensor, group=None, reproducible: bool = Fa
 
 
 def run_partitioned(evaluate: Callable[[int], torch.Tensor], n_slices: int, world: int, rank: int,
-                    group=None, reproducible: bool = False) -> torch.Tensor:
+                    group=None, reproducible: bool = False,
+                    zeros: Callable[[], torch.Tensor] | None = None) -> torch.Tensor:
     """Evaluate this rank's slices with ``evaluate(slice_id)`` (device tensor),
-    fold them in slice order, then all-reduce.  Returns the global sum."""
+    fold them in slice order, then all-reduce.  Returns the global sum.  A
+    rank that owns no slice joins the collective with ``zeros()``."""
     acc = None
     for sid in partition(n_slices, world, rank):
         part = evaluate(sid)
         acc = part.clone() if acc is None else acc.add_(part)
     if acc is None:
-        # a rank without slices still joins the collective with zeros
-        probe = evaluate(0)
-        acc = torch.zeros_like(probe)
+        if zeros is None:
+            raise ValueError(f"rank {rank} owns no slice of {n_slices}: pass zeros= for the output shape")
+        acc = zeros()
     return allreduce_partial(acc, group, reproducible)
+
+
+def _world_rank(world, rank, group):
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    return world, rank
+
+
+def accumulate_rank_units(executor, unit_ids: Sequence[int], world: int | None = None, rank: int | None = None,
+                          acc=None, group=None):
+    """This rank's share (round-robin, ``partition``) of ``unit_ids`` folded
+    into ``acc`` on the device -- no collective.  A unit is a slice
+    (:class:`SliceExecutor`) or a reuse program (:class:`ReuseRunner`).  Used
+    by the bench, which accumulates several steps and all-reduces once."""
+    world, rank = _world_rank(world, rank, group)
+    ids = list(unit_ids)
+    mine = [ids[i] for i in partition(len(ids), world, rank)]
+    if mine:
+        acc = executor.run(mine, acc)
+    elif acc is None:
+        acc = executor.zeros()
+    return acc
 
 
 def run_slices_distributed(executor, world: int | None = None, rank: int | None = None,
                            slice_ids: Sequence[int] | None = None, group=None, reproducible: bool = False):
     """Distributed sum of a :class:`~paper_2504_09186_b200.execute.SliceExecutor`
-    over all (or the given) slices; returns the output tensor on every rank."""
-    if world is None:
-        world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if rank is None:
-        rank = dist.get_rank(group) if dist.is_initialized() else 0
-    ids = list(range(executor.spec.n_subtasks)) if slice_ids is None else list(slice_ids)
-    mine = [ids[i] for i in partition(len(ids), world, rank)]
-    total = executor.run(mine) if mine else None
-    if total is None:
-        total = executor.run([ids[0]])
-        total.data.zero_()
+    (or ``ReuseRunner``) over all (or the given) units; returns the output
+    tensor on every rank."""
+    world, rank = _world_rank(world, rank, group)
+    ids = list(range(executor.n_units)) if slice_ids is None else list(slice_ids)
+    total = accumulate_rank_units(executor, ids, world, rank, None, group)
     allreduce_partial(total.data, group, reproducible)
     return executor.finish(total)

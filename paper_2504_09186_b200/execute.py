@@ -446,6 +446,15 @@ def run_reuse_open(net: TensorNetwork, t: ContractionTree, rs: ReuseSchedule,
     return permute(total, [by[l] for l in output_order])
 
 
+def _zeros_root(eng: Engine, s: LinearSchedule) -> DenseTensor:
+    """A zero tensor shaped like the schedule's root (open legs are never
+    sliced), without evaluating anything: what a rank that owns no slices
+    contributes to the all-reduce."""
+    idx = tuple(s.steps[-1].indices) if s.steps else ()
+    data = torch.zeros(tuple(ix.dim for ix in idx), dtype=DTYPES[eng.precision], device="cuda")
+    return DenseTensor.__new__(DenseTensor)._init_raw(idx, data)
+
+
 class ReuseRunner:
     """Spindle-reuse scheduler for open outputs on one device: the reuse
     program of ``rs`` (reference ``reuse.py:298-514`` / ``execute.py:233-313``)
@@ -531,6 +540,14 @@ class ReuseRunner:
             return total
         by = {ix.label: ix for ix in total.indices}
         return permute(total, [by[l] for l in self.output_order])
+
+    def zeros(self) -> DenseTensor:
+        return _zeros_root(self.eng, self.s)
+
+    @property
+    def n_units(self) -> int:
+        """Units of work the distributed scheduler deals out (programs)."""
+        return self.n_programs
 
 
 class SliceExecutor:
@@ -626,6 +643,14 @@ class SliceExecutor:
             return total
         by = {ix.label: ix for ix in total.indices}
         return permute(total, [by[l] for l in self.output_order])
+
+    def zeros(self) -> DenseTensor:
+        return _zeros_root(self.eng, self.s)
+
+    @property
+    def n_units(self) -> int:
+        """Units of work the distributed scheduler deals out (slices)."""
+        return self.spec.n_subtasks
 
 
 def _proj_cost(s: LinearSchedule, pos: int, dims: dict[str, int]) -> int:

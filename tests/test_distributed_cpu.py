@@ -73,3 +73,70 @@ def test_partition_covers_every_slice_once():
         assert got == list(range(37))
     with pytest.raises(ValueError):
         partition(4, 2, 2)
+
+
+class _RootsExecutor:
+    """Executor stand-in: unit i's root is the reference's golden slice root."""
+
+    def __init__(self, roots):
+        self.roots = roots
+        self.n_units = len(roots)
+        self.calls = []
+
+    def run(self, ids, acc=None):
+        for i in ids:
+            self.calls.append(i)
+            acc = self.roots[i].clone() if acc is None else acc + self.roots[i]
+        return _Wrap(acc)
+
+    def zeros(self):
+        return _Wrap(torch.zeros_like(self.roots[0]))
+
+    def finish(self, total):
+        return total.data
+
+
+class _Wrap:
+    def __init__(self, data):
+        self.data = data.data if isinstance(data, _Wrap) else data
+
+    def __add__(self, other):
+        return _Wrap(self.data + other)
+
+    def clone(self):
+        return _Wrap(self.data.clone())
+
+
+def _worker_units(rank, world, port, n_units, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2504_09186_b200.distributed import run_slices_distributed
+
+    g = load_golden("sliced")
+    roots = [torch.from_numpy(arr(it["data"]).astype(np.complex128)) for it in g["open_net"]["per_slice"]]
+    ex = _RootsExecutor(roots)
+    total = run_slices_distributed(ex, world, rank, slice_ids=list(range(n_units)))
+    out_q.put((rank, ex.calls, total.numpy()))
+    dist.destroy_process_group()
+
+
+def test_three_ranks_two_units_empty_rank_joins_with_zeros():
+    """More ranks than units: rank 2 owns nothing, evaluates nothing and
+    contributes zeros of the root's shape to the all-reduce."""
+    g = load_golden("sliced")
+    roots = [arr(it["data"]).astype(np.complex128) for it in g["open_net"]["per_slice"]]
+    want = roots[0] + roots[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_units, args=(r, 3, port, 2, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [calls for _, calls, _ in results] == [[0], [1], []]
+    for _, _, total in results:
+        assert rel_l2(total, want) < 1e-12
