@@ -163,3 +163,27 @@ def test_slice_map_mixed_radix():
     for sid in (0, 1, 5, len(keys) - 1):
         asn = spec.assignment(sid)
         assert tuple(asn[l] for l in spec.labels) == keys[sid]
+
+
+def test_c4_reuse_plan_max_k12_matches_reference():
+    """C4 spindle plan at the reference default max_k = 12 (reference
+    ``reuse.py:530-573`` + ``plan_spindle``): nested / outer labels, the
+    34,296-action program, predicted multiplies and peak bytes identical to the
+    reference's (fixture written by ``oracle/gen_golden.py plan_c4_reuse``)."""
+    path = GOLDEN / "plan_c4_reuse.json.gz"
+    if not path.exists():
+        pytest.skip("plan_c4_reuse fixture not generated")
+    g = load_golden("plan_c4_reuse")
+    r = g["reuse"]
+    wl = workloads.CircuitWorkload(g["rows"], g["cols"], g["cycles"], g["seed"], len(g["open"]))
+    t = greedy_path(wl.network(), 0)
+    spec = select_slices(t, g["max_rank"], 64, 0)
+    part = choose_reuse_subset(t, spec, None, r["max_k"])
+    assert part.nested_labels == r["nested"]
+    assert [e.index.label for e in part.outer] == r["outer"]
+    assert _steps(part.schedule) == r["steps"]
+    assert json.loads(part.spec.to_json()) == r["spec"]
+    rs, rep = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    assert [a.to_obj() for a in rs.actions] == r["actions"]
+    assert rep.predicted_multiplies == r["report"]["predicted_multiplies"]
+    assert rep.predicted_peak_bytes == r["report"]["predicted_peak_bytes"]
