@@ -266,9 +266,10 @@ def _spiky_pair(m_bits, k_bits, n_bits, spike, seed, shuffle):
     if shuffle:  # permuted operands: exercises the fused gather + split path
         rng = np.random.default_rng(seed)
         pa, pb = rng.permutation(len(la)), rng.permutation(len(lb))
-        a_data = a.reshape((2,) * len(la)).permute(*pa.tolist()).contiguous().reshape(-1)
-        b_data = b.reshape((2,) * len(lb)).permute(*pb.tolist()).contiguous().reshape(-1)
-        la, lb = [la[i] for i in pa], [lb[i] for i in pb]
+        la2, lb2 = [la[i] for i in pa], [lb[i] for i in pb]
+        a_data = devcheck.permute((la, (2,) * len(la), a_data), la2)[2]
+        b_data = devcheck.permute((lb, (2,) * len(lb), b_data), lb2)[2]
+        la, lb = la2, lb2
     out = [f"a{i}" for i in range(m_bits)] + [f"b{i}" for i in range(n_bits)]
     return la, a_data, lb, b_data, out, want
 
