@@ -294,6 +294,7 @@ def test_auto_dynamic_range_on_k2_shape(cuda_ready, spike):
 
     la, ad, lb, bd, out, want = _spiky_pair(15, 11, 8, spike, 8, True)
     ia, ib = [Index(l) for l in la], [Index(l) for l in lb]
+    ad, bd = ad.reshape((2,) * len(la)), bd.reshape((2,) * len(lb))
     plan = plan_for(ia, ad.stride(), ib, bd.stride(), _lib.C64, [Index(l) for l in out])
     assert plan.variant == _lib.VARIANT_TC3XF16
     got = contract_into(plan, ad, bd)
