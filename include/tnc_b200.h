@@ -135,19 +135,26 @@ int tnc_contract_split(const tnc_plan* plan, int32_t blocks, int32_t group, cons
                        void* stream);
 
 /* ---- K4: step fusion (absorb a chain of small gates into a big tensor) -----
- * T (rank t_rank in [12, 62], contiguous complex64, dims all 2) absorbs n_gates
- * two-leg gates sequentially; gates[g] is a HOST pointer to 16 complex64 values
- * laid out (out_a,out_b,in_a,in_b) acting on T legs (axes[2g], axes[2g+1]) --
- * positions in the CURRENT leg order.  Reference semantics of
- * contract_pair(T, G): the two contracted legs are removed and the gate's out
- * legs are appended at the end.  The output is written in the final leg order
- * after all gates; t_out must not alias t_in.  Workspace: one tensor-sized
- * buffer when the chain needs more than one pass (see _workspace). */
+ * T (rank t_rank in [13, 62], contiguous complex64, dims all 2) absorbs n_gates
+ * two-leg gates sequentially.  gates[g] is a DEVICE pointer to the gate's 16
+ * complex64 values; gate_strides[4g .. 4g+3] are the element strides of its
+ * (out_a, out_b, in_a, in_b) legs, so any leg order / strided view of a
+ * rank-4 gate tensor works without a copy.  The gate acts on T legs
+ * (axes[2g] = in_a, axes[2g+1] = in_b) -- positions in the CURRENT leg order.
+ * Reference semantics of contract_pair(T, G) (contract.py:149-165): the two
+ * contracted legs are removed and the gate's out legs are appended at the end.
+ * The output is written in the final leg order after all gates; t_out must
+ * not alias t_in.  Workspace (tnc_absorb_chain_workspace): the group unitary
+ * table, plus one tensor-sized buffer when the chain needs more than one HBM
+ * pass.  The gate values stay on the device (no host round trip, no sync). */
 int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,
-                     const void* const* gates, const int32_t* axes, void* workspace,
-                     size_t workspace_bytes, void* stream);
+                     const void* const* gates, const int64_t* gate_strides, const int32_t* axes,
+                     void* workspace, size_t workspace_bytes, void* stream);
 int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* axes,
                                size_t* workspace_bytes);
+/* HBM passes and 3-axis gate groups the planner uses for this chain. */
+int tnc_absorb_chain_info(int32_t t_rank, int32_t n_gates, const int32_t* axes, int32_t* passes,
+                          int32_t* groups);
 
 /* ---- K6: accumulation ----------------------------------------------------- */
 /* y[i] += x[i] for n complex elements. */

@@ -69,8 +69,10 @@ SIGNATURES = {
     "tnc_contract": (ctypes.c_int, [_P, _P, _P, _P, _P, _SZ, _P]),
     "tnc_contract_split_workspace": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_SZ)]),
     "tnc_contract_split": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _SZ, _P]),
-    "tnc_absorb_chain": (ctypes.c_int, [_I32, _P, _P, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I32),
-                                        _P, _SZ, _P]),
+    "tnc_absorb_chain": (ctypes.c_int, [_I32, _P, _P, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64),
+                                        ctypes.POINTER(_I32), _P, _SZ, _P]),
+    "tnc_absorb_chain_info": (ctypes.c_int, [_I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                                             ctypes.POINTER(_I32)]),
     "tnc_absorb_chain_workspace": (ctypes.c_int, [_I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_SZ)]),
     "tnc_axpy": (ctypes.c_int, [_I32, _I64, _P, _P, _P]),
     "tnc_launch_count": (ctypes.c_int64, []),

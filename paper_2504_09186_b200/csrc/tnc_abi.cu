@@ -915,10 +915,22 @@ int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* a
 }
 
 int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,
-                     const void* const* gates, const int32_t* axes, void* workspace,
-                     size_t workspace_bytes, void* stream) {
-  return absorb_chain_launch(t_rank, t_in, t_out, n_gates, gates, axes, workspace,
+                     const void* const* gates, const int64_t* gate_strides, const int32_t* axes,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_gates > 0 && (!gates || !gate_strides || !axes)) TNC_RET(TNC_ERR_INVALID, "null argument");
+  if (!t_in || !t_out || t_in == t_out) TNC_RET(TNC_ERR_INVALID, "absorb: t_in / t_out null or aliased");
+  return absorb_chain_launch(t_rank, t_in, t_out, n_gates, gates, gate_strides, axes, workspace,
                              workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int tnc_absorb_chain_info(int32_t t_rank, int32_t n_gates, const int32_t* axes, int32_t* passes,
+                          int32_t* groups) {
+  if (!passes || !groups || (n_gates > 0 && !axes)) TNC_RET(TNC_ERR_INVALID, "null argument");
+  int p = 0, g = 0;
+  TNC_TRY(absorb_chain_passes(t_rank, n_gates, axes, &p, &g));
+  *passes = p;
+  *groups = g;
+  return TNC_OK;
 }
 
 }  // extern "C"

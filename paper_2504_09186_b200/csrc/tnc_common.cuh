@@ -180,8 +180,9 @@ int stream_launch(const StreamPlan* sp, const void* x, const void* y, void* c, c
 
 // K4 step fusion (tnc_absorb.cu)
 int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t* bytes);
-int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates,
-                        const void* const* gates, const int32_t* axes, void* workspace,
+int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, const void* const* gates,
+                        const int64_t* gate_strides, const int32_t* axes, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream);
+int absorb_chain_passes(int t_rank, int n_gates, const int32_t* axes, int* passes, int* groups);
 
 }  // namespace tnc

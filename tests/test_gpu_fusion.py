@@ -21,7 +21,8 @@ def _chain(rank, n_gates, seed):
     return t_labels, data, gates, t, gs
 
 
-@pytest.mark.parametrize("rank,n_gates,seed", [(14, 16, 1), (16, 5, 2), (18, 16, 3), (12, 3, 4)])
+@pytest.mark.parametrize("rank,n_gates,seed", [(14, 16, 1), (16, 5, 2), (18, 16, 3), (12, 3, 4), (13, 16, 5),
+                                               (13, 40, 6), (20, 0, 7), (21, 64, 8), (15, 1, 9)])
 def test_absorb_chain_vs_oracle(cuda_ready, rank, n_gates, seed):
     from paper_2504_09186_b200.fusion import absorb_chain
 
@@ -55,3 +56,42 @@ def test_absorb_chain_rejects_bad_gate(cuda_ready):
     bad = DenseTensor([Index("x"), Index("y"), Index("z"), Index("w0")], np.ones(16, np.complex64))
     with pytest.raises(ContractionError):
         absorb_chain(t, [bad])
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_absorb_chain_strided_gate_views(cuda_ready, seed):
+    """Gates given as permuted (non-contiguous) views of their storage: the
+    kernel reads them through the leg strides, no copies."""
+    from paper_2504_09186_b200 import DenseTensor, Index, execute  # noqa: F401  (DenseTensor._init_raw)
+    from paper_2504_09186_b200.fusion import absorb_chain
+
+    t_labels, data, gates, t, _ = _chain(17, 12, 30 + seed)
+    rng = np.random.default_rng(seed)
+    gs = []
+    ref = (tuple(t_labels), (2,) * 17, data.astype(np.complex128))
+    for ia, ib, oa, ob, u in gates:
+        perm = rng.permutation(4)
+        legs = [oa, ob, ia, ib]
+        base = torch.from_numpy(u.reshape(2, 2, 2, 2)).cuda()
+        view = base.permute(*perm.tolist())  # strided view, legs in permuted order
+        gs.append(DenseTensor.__new__(DenseTensor)._init_raw(tuple(Index(legs[i]) for i in perm), view))
+        gdata = u.reshape(2, 2, 2, 2).transpose(perm).reshape(-1).astype(np.complex128)
+        ref = tncref.contract(ref, (tuple(legs[i] for i in perm), (2, 2, 2, 2), gdata))
+    got = absorb_chain(t, gs)
+    assert list(got.labels) == list(ref[0])
+    assert rel_l2(got.numpy(), ref[2]) <= 1e-5
+
+
+def test_c2_plan_is_two_passes(cuda_ready):
+    from paper_2504_09186_b200 import DenseTensor, Index, execute  # noqa: F401
+    from paper_2504_09186_b200.fusion import chain_info, plan_chain
+    from paper_2504_09186_b200.workloads import C2
+
+    t_labels, data, gates = C2.build()
+    del data
+    t = DenseTensor.__new__(DenseTensor)._init_raw(tuple(Index(l) for l in t_labels), torch.zeros(1))
+    gs = [DenseTensor.__new__(DenseTensor)._init_raw((Index(oa), Index(ob), Index(ia), Index(ib)),
+                                                     torch.zeros(2, 2, 2, 2)) for ia, ib, oa, ob, u in gates]
+    axes, _, _ = plan_chain(t, gs)
+    passes, groups = chain_info(30, axes)
+    assert passes == 2, (passes, groups)
