@@ -1,5 +1,6 @@
 // K4: step fusion -- a chain of two-leg gate absorptions into one resident
-// tensor, with the gate math on tensor cores, in the fewest HBM passes.
+// tensor in the fewest HBM passes, the gate math overlapped with the HBM
+// streams.
 //
 // Reference semantics: successive contract_pair(T, G) along a stem
 // (execute.py:137-178 over tree.py:278-384 stems; contract.py:149-165):
@@ -18,25 +19,25 @@
 //    its axes).  Between passes the intermediate layout is free: its 3 fastest
 //    axes ("link") are tile axes of both passes (coalesced writes and reads)
 //    and the next pass's tile axes come next (its reads are contiguous runs).
-//    C2 (16 random gates on a rank-30 tensor): 2 passes (was 3 with 12-bit
-//    tiles and in-order sections).
-//  * Math.  Within a pass the gates are grouped on 3 tile axes and multiplied
-//    into one 8x8 complex unitary per group (device kernel, double, no host
-//    round trip for the gate values).  A group is applied to the tile as the
-//    real GEMM  [1024 rows x 16] x [16 x 16]  on mma.sync.m16n8k16 (fp16 in,
-//    fp32 accumulate) with a 3-product split: each 8-element row is scaled by
-//    a power of two to the top of the fp16 range (f16_row_exponent), split
-//    into hi + lo halves, and  lo*U_hi + hi*U_lo + hi*U_hi  are accumulated,
-//    then the row scale is undone.  The A fragment of a thread is 4 complex
-//    elements (rows g, g+8 x cols q, q+4) and its D fragment is the same 4
-//    positions, so every group is an in-place smem read-modify-write: 16 B of
-//    smem traffic and 192 tensor flops per element per group (vs 64 FP32 FMA
-//    per element for the same 3 gates on CUDA cores).
+//    C2 (16 random gates on a rank-30 tensor): 2 passes (3 with in-order
+//    sections of 12-bit tiles).
+//  * Pipeline.  One persistent CTA per SM, warp-specialised over a ring of 3
+//    tile buffers: 4 memory warps gather tile k (cp.async, mbarrier-tracked)
+//    and store tile k-1 while 8 math warps apply the pass's gates to the tile
+//    in between.  A pure copy pass runs at 6.4 TB/s (99 % of the measured HBM
+//    peak), so the pass time is max(HBM, gate math).
+//  * Math.  Gates are grouped on <= 5 tile axes; each math thread holds a
+//    32-element register cube of the group's axes (256 threads x 32 = the
+//    tile) and applies the group's 4x4 gates with packed FP32 FMAs (FFMA2:
+//    2 per complex MAC).  The gate tables (oriented (re, re, -im, im) rows)
+//    are built on the device from the caller's device gate tensors: no host
+//    round trip.  (A tensor-core variant -- 16x16 group unitaries on
+//    mma.sync with a 3xFP16 split -- was correct but issue-bound at ~2 ms
+//    per group: commit d9b05fc.)
 //  * Banks.  8-byte smem slots are XOR-swizzled (swz); a tile bit's bank class
 //    is (bit mod 4).  The host places tile axes so that the 4 fastest load
-//    axes, the 4 fastest store axes, and each group's lane bits (2 column +
-//    2 row bits) cover 4 distinct classes: every half-warp access is
-//    conflict-free.
+//    axes and the 4 fastest store axes each cover the 4 classes, and picks a
+//    cube's lane bits with distinct classes.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -55,36 +56,30 @@ using namespace tc5;
 
 constexpr int kTB = 13;                       // tile bits
 constexpr int kTile = 1 << kTB;               // 8192 complex64 = 64 KB
-constexpr int kMathThreads = 256;             // 8 math warps (tensor-core group application)
+constexpr int kMathThreads = 256;             // 8 math warps: one 32-element cube per thread
 constexpr int kMemThreads = 128;              // 4 memory warps (HBM <-> smem)
 constexpr int kThreads = kMathThreads + kMemThreads;
 constexpr int kBufs = 3;                      // tile ring: loading / math / storing
 constexpr int kMemPer = kTile / kMemThreads;  // 64 elements per memory thread per tile
 constexpr int kMemThrBits = 7;
-constexpr int kMaxGroups = 5;                 // groups per pass (B fragments in smem: 6 KB each)
+constexpr int kCubeBits = 5;
+constexpr int kCube = 1 << kCubeBits;
+constexpr int kMaxGroups = 24;                // groups per pass
+constexpr int kMaxPassGates = 64;             // gates per pass (tables in smem: 256 B each)
 constexpr int kMaxChainGates = 512;
-constexpr int kMaxAllGroups = 512;            // groups over all passes (fragment table)
-constexpr int kGroupWords = 48;               // B-fragment u32 per lane per group
 
-// A group is a 16x16 complex unitary on 4 tile bits (gates on up to 4 axes
-// multiplied together; a smaller group is padded with identity axes),
-// applied to the tile viewed as [512 rows x 16] on mma.sync.m16n8k16:
-// K = 32 real (2 k-steps), N = 32 real (4 n8 tiles), 4 m16 tiles per warp.
-// B fragments per lane: 2 regs x 4 n-tiles x 2 k-steps x (B_hi, -B_hi, -B_lo) = 48 u32.
 struct GroupParams {
-  int frag_off;      // offset of the group's fragments in the table, in units of 32 u32
-  int lane_slot[5];  // slot vectors of lane bits 0..4 = (q0, q1, g0, g1, g2)
-  int warp_slot[3];  // math warp id bits
-  int iter[4];       // slot XOR of m16-tile iteration m
-  int h_slot;        // row + 8
-  int q2_slot;       // column + 4
-  int q3_slot;       // column + 8 (second k-step)
+  int cube_slot[kCubeBits];  // slot vectors of the cube (register-index) bits
+  int lane_slot[5];          // lane bits
+  int warp_slot[3];          // math warp id bits
+  int g_first, g_last;       // the group's gates in the pass's gate list
 };
 
 struct AbsorbParams {
   int n_outer;
   int n_groups;
-  int frag_base;     // the pass's first group in the fragment table (units of 32 u32)
+  int n_gates;               // gates of this pass
+  int table_base;            // the pass's first gate in the device table
   int64_t n_tiles;
   // memory-thread enumeration e = mt + 128 i: offset = thread part + [i] part
   int64_t in_bit[kMemThrBits];
@@ -96,20 +91,17 @@ struct AbsorbParams {
   int64_t out_i[kMemPer];
   int out_slot_i[kMemPer];
   GroupParams g[kMaxGroups];
+  int gate_local[kMaxPassGates];    // 8 * (cube bit of in_a) + cube bit of in_b, a < b
   int64_t outer_in[TNC_MAX_RANK];   // outer bit k of the tile index: input / output stride
   int64_t outer_out[TNC_MAX_RANK];
 };
 
-// Fragment-table job: group k (width w_k column bits, fragments at u32 offset
-// off_k * 32) multiplies gates grp_gate[grp_first[k] .. grp_first[k+1]) in
-// order; gate j acts on column bits (ca, cb).
-struct FragParams {
-  int n_groups;
-  int grp_first[kMaxAllGroups + 1];
-  int grp_off[kMaxAllGroups];
-  signed char grp_w[kMaxAllGroups];
-  short grp_gate[kMaxChainGates];
-  signed char grp_ca[kMaxChainGates], grp_cb[kMaxChainGates];
+// Device gate tables: entry j = 16 float4 (U[o][i] as (re, re, -im, im)) of
+// chain gate src[j], oriented so that its in_a axis is the lower cube bit.
+struct TableParams {
+  int n;
+  short src[kMaxChainGates];
+  signed char swap[kMaxChainGates];
   const float2* gate[kMaxChainGates];
   int64_t gstride[kMaxChainGates][4];  // element strides of the (out_a, out_b, in_a, in_b) legs
 };
@@ -120,216 +112,96 @@ __device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gmem_sr
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_dst), "l"(gmem_src) : "memory");
 }
 
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-
 typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk(float2 v) {
+__device__ __forceinline__ u64 as_u64(float2 v) {
   u64 r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
   return r;
 }
-__device__ __forceinline__ float2 upk(u64 r) {
+__device__ __forceinline__ float2 as_f2(u64 r) {
   float2 v;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
   return v;
 }
-// packed fp32x2 FMA (one issue slot for a complex element)
+__device__ __forceinline__ u64 bcast(float x) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+  return r;
+}
+// packed fp32x2 FMA (sm_100 FFMA2): one issue slot for both halves
 __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
   u64 r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
 
-
-
-__device__ __forceinline__ float amax2(float2 a, float2 b) {
-  return fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(b.x), fabsf(b.y)));
+// acc += u * x as two FFMA2 with no broadcast moves: the table holds
+// (u.re, u.re, -u.im, u.im) and xs = (x.im, x.re) is swapped once per element
+//   acc += (u.re, u.re) * (x.re, x.im) + (-u.im, u.im) * (x.im, x.re)
+__device__ __forceinline__ u64 cmac(u64 acc, float4 u, u64 x, u64 xs) {
+  acc = ffma2(as_u64(make_float2(u.x, u.y)), x, acc);
+  return ffma2(as_u64(make_float2(u.z, u.w)), xs, acc);
 }
 
-// Group unitaries -> per-lane mma B fragments (hi / lo fp16) in global memory.
-// One warp per group; lane 0 multiplies the embedded gates in double.
-__global__ void absorb_frag_kernel(const FragParams p, uint32_t* __restrict__ table) {
-  __shared__ double mr[16][16], mi[16][16], nr[16][16], ni[16][16];
-  const int grp = blockIdx.x;
-  const int lane = threadIdx.x;
-  const int w = p.grp_w[grp], D = 1 << w;
-  for (int e = lane; e < D * D; e += 32) {
-    mr[e / D][e % D] = (e / D == e % D) ? 1.0 : 0.0;
-    mi[e / D][e % D] = 0.0;
-  }
-  __syncwarp();
-  for (int j = p.grp_first[grp]; j < p.grp_first[grp + 1]; ++j) {
-    const int gi = p.grp_gate[j], ca = p.grp_ca[j], cb = p.grp_cb[j];
-    const float2* u = p.gate[gi];
-    const int64_t* st = p.gstride[gi];
-    const int keep = ~((1 << ca) | (1 << cb));
-    for (int e = lane; e < D * D; e += 32) {
-      const int o = e / D, i = e % D;
-      const int oa = (o >> ca) & 1, ob = (o >> cb) & 1;
-      double sr = 0.0, si = 0.0;
-      for (int q = 0; q < 4; ++q) {  // embedded gate G[o][k]: k differs from o only on (ca, cb)
-        const int ka = q >> 1, kb = q & 1;
-        const int k = (o & keep) | (ka << ca) | (kb << cb);
-        const float2 g = u[oa * st[0] + ob * st[1] + ka * st[2] + kb * st[3]];
-        sr += g.x * mr[k][i] - g.y * mi[k][i];
-        si += g.x * mi[k][i] + g.y * mr[k][i];
-      }
-      nr[o][i] = sr;
-      ni[o][i] = si;
+// 4x4 gate on cube bits (LA = in_a < LB = in_b) of a 32-element register cube
+template <int LA, int LB>
+__device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* u) {
+  float4 uu[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) uu[i] = u[i];  // shared memory, broadcast
+#pragma unroll
+  for (int s = 0; s < kCube; ++s) {
+    if ((s >> LA) & 1) continue;
+    if ((s >> LB) & 1) continue;
+    const int idx[4] = {s, s | (1 << LB), s | (1 << LA), s | (1 << LA) | (1 << LB)};
+    u64 x[4], xs[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] = as_u64(v[idx[i]]);
+      xs[i] = as_u64(make_float2(v[idx[i]].y, v[idx[i]].x));
     }
-    __syncwarp();
-    for (int e = lane; e < D * D; e += 32) {
-      mr[e / D][e % D] = nr[e / D][e % D];
-      mi[e / D][e % D] = ni[e / D][e % D];
-    }
-    __syncwarp();
-  }
-  // real B[k][n], k = 2i + d (input column i, d = re/im), n = 2o + c:
-  //   B[2i][2o] = Mr[o][i], B[2i+1][2o] = -Mi[o][i], B[2i][2o+1] = Mi[o][i], B[2i+1][2o+1] = Mr[o][i]
-  auto bval = [&](int k, int n) -> double {
-    const int i = k >> 1, d = k & 1, o = n >> 1, c = n & 1;
-    if (c == 0) return d == 0 ? mr[o][i] : -mi[o][i];
-    return d == 0 ? mi[o][i] : mr[o][i];
-  };
-  const int n_tiles = D / 4, k_steps = D / 8;
-  uint32_t* out = table + static_cast<int64_t>(p.grp_off[grp]) * 32 + lane * (6 * n_tiles * k_steps);
-  const int q = lane & 3, gq = lane >> 2;
-  // layout per lane: [set][n-tile][k-step][2 regs], sets (B_hi, -B_hi, -B_lo):
-  // the tile side is split as (-hi, lo) so that  lo*B_hi + (-hi)*(-B_lo) +
-  // (-hi)*(-B_hi)  is the 3-product sum (see split_nhi)
-  for (int hl = 0; hl < 3; ++hl)
-    for (int nt = 0; nt < n_tiles; ++nt)
-      for (int ks = 0; ks < k_steps; ++ks) {
-        const int n = 8 * nt + gq;
-        const int kk[4] = {16 * ks + 2 * q, 16 * ks + 2 * q + 1, 16 * ks + 2 * q + 8, 16 * ks + 2 * q + 9};
-        __half h[4];
-        for (int j = 0; j < 4; ++j) {
-          const double v = bval(kk[j], n);
-          const __half hi = __double2half(v);
-          const __half lo = __double2half(v - static_cast<double>(__half2float(hi)));
-          h[j] = hl == 0 ? hi : hl == 1 ? __hneg(hi) : __hneg(lo);
-        }
-        uint32_t* o = out + 2 * ((hl * n_tiles + nt) * k_steps + ks);
-        o[0] = h2_bits(__halves2half2(h[0], h[1]));
-        o[1] = h2_bits(__halves2half2(h[2], h[3]));
-      }
-}
-
-// Tile-side split of one complex element (x * 2^-e as fp16 pieces), 5 issue
-// slots: t = x*s + M rounds x*s to a multiple of 16 (M = 1.5 * 2^27; the row
-// max is scaled into [2^14, 2^15), so the rounded value has <= 11 significant
-// bits and is exact in fp16), nh = M - t = -hi exactly, lo = x*s - hi exactly
-// (fp16-rounded to 2^-22 of the row max).  Returns (-hi, lo) as half2 pairs.
-constexpr u64 kM2 = 0x4d4000004d400000ull;    // (1.5 * 2^27, 1.5 * 2^27)
-constexpr u64 kNeg1 = 0xbf800000bf800000ull;  // (-1, -1)
-__device__ __forceinline__ void split_nhi(float2 x, u64 s, uint32_t& nhi, uint32_t& lo) {
-  const u64 xv = pk(x);
-  const u64 t = ffma2(xv, s, kM2);
-  const u64 nh = ffma2(t, kNeg1, kM2);
-  const u64 l = ffma2(xv, s, nh);
-  nhi = h2_bits(__float22half2_rn(upk(nh)));
-  lo = h2_bits(__float22half2_rn(upk(l)));
-}
-
-__device__ __forceinline__ u64 pow2_pair(uint32_t bits) { return (static_cast<u64>(bits) << 32) | bits; }
-
-// One group on the tile: per m16 tile a thread holds rows (g, g+8) x columns
-// (q, q+4, q+8, q+12); k-step s covers columns 8s..8s+7.  Two m16 tiles are
-// processed together (independent chains for latency hiding; their 4 row
-// exponents share one pair of shuffles).
-__device__ __forceinline__ void apply_group(float2* tile, const GroupParams& gp, const uint32_t* fr,
-                                            int base) {
-  uint32_t fb[48];  // [set: B_hi, -B_hi, -B_lo][n-tile 4][k-step 2][2]
 #pragma unroll
-  for (int v = 0; v < 12; ++v) {
-    const uint4 t = reinterpret_cast<const uint4*>(fr)[v];  // shared memory
-    fb[4 * v + 0] = t.x;
-    fb[4 * v + 1] = t.y;
-    fb[4 * v + 2] = t.z;
-    fb[4 * v + 3] = t.w;
-  }
-  // loop-invariant slot vectors in registers (no indexed param loads in the loop)
-  const int h_slot = gp.h_slot, q2_slot = gp.q2_slot, q3_slot = gp.q3_slot;
-  const int it_slot[4] = {gp.iter[0], gp.iter[1], gp.iter[2], gp.iter[3]};
-#pragma unroll 1
-  for (int mp = 0; mp < 4; mp += 2) {
-    int sl[2][8];  // element e = h + 2 j + 4 s : row g + 8h, column q + 4j + 8s
-    float2 x[2][8];
+    for (int o = 0; o < 4; ++o) {
+      u64 acc = 0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      sl[u][0] = base ^ (mp ? it_slot[2 + u] : it_slot[u]);
-      sl[u][1] = sl[u][0] ^ h_slot;
-      sl[u][2] = sl[u][0] ^ q2_slot;
-      sl[u][3] = sl[u][1] ^ q2_slot;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sl[u][4 + e] = sl[u][e] ^ q3_slot;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) x[u][e] = tile[sl[u][e]];
-    }
-    // row maxima -> 4 exponent bytes, quad max with two shuffles
-    uint32_t ex = 0;
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float mx = fmaxf(amax2(x[u][h], x[u][h + 2]), amax2(x[u][h + 4], x[u][h + 6]));
-        ex |= (__float_as_uint(mx) >> 23) << (8 * (2 * u + h));
-      }
-    ex = __vmaxu4(ex, __shfl_xor_sync(0xffffffffu, ex, 1));
-    ex = __vmaxu4(ex, __shfl_xor_sync(0xffffffffu, ex, 2));
-    ex = __vmaxu4(ex, 0x0f0f0f0fu);
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      u64 sc[2], un[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t E = (ex >> (8 * (2 * u + h))) & 0xffu;
-        sc[h] = pow2_pair((268u - E) << 23);  // 2^(141 - E): row max -> [2^14, 2^15)
-        un[h] = pow2_pair((E - 14u) << 23);   // 2^(E - 141)
-      }
-      uint32_t ah[2][4], al[2][4];
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) split_nhi(x[u][4 * ks + r], sc[r & 1], ah[ks][r], al[ks][r]);
-      // two accumulation chains per n-tile (small terms / main term), summed
-      // after: halves the dependent-HMMA chain length
-      float d[4][4], c[4][4];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-        c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const int o = 2 * (nt * 2 + ks);
-          mma16816(c[nt], al[ks], fb[o], fb[o + 1]);            // lo * B_hi
-          mma16816(d[nt], ah[ks], fb[16 + o], fb[16 + o + 1]);  // (-hi) * (-B_hi)
-          mma16816(c[nt], ah[ks], fb[32 + o], fb[32 + o + 1]);  // (-hi) * (-B_lo)
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) d[nt][v] += c[nt][v];
-      }
-      // output column o = 4 nt + q = q + 4 j + 8 s with j = nt & 1, s = nt >> 1
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int e0 = 2 * (nt & 1) + 4 * (nt >> 1);
-        tile[sl[u][e0]] = upk(ffma2(pk(make_float2(d[nt][0], d[nt][1])), un[0], 0ull));
-        tile[sl[u][e0 + 1]] = upk(ffma2(pk(make_float2(d[nt][2], d[nt][3])), un[1], 0ull));
-      }
+      for (int i = 0; i < 4; ++i) acc = cmac(acc, uu[o * 4 + i], x[i], xs[i]);
+      v[idx[o]] = as_f2(acc);
     }
   }
 }
 
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void apply_gate(float2 (&v)[kCube], int local, const float4* u) {
+  switch (local) {
+    case 8 * 0 + 1: apply_local<0, 1>(v, u); break;
+    case 8 * 0 + 2: apply_local<0, 2>(v, u); break;
+    case 8 * 0 + 3: apply_local<0, 3>(v, u); break;
+    case 8 * 0 + 4: apply_local<0, 4>(v, u); break;
+    case 8 * 1 + 2: apply_local<1, 2>(v, u); break;
+    case 8 * 1 + 3: apply_local<1, 3>(v, u); break;
+    case 8 * 1 + 4: apply_local<1, 4>(v, u); break;
+    case 8 * 2 + 3: apply_local<2, 3>(v, u); break;
+    case 8 * 2 + 4: apply_local<2, 4>(v, u); break;
+    case 8 * 3 + 4: apply_local<3, 4>(v, u); break;
+    default: break;
+  }
+}
+
+// Gate tables from the caller's device gate tensors (one thread per entry).
+__global__ void absorb_table_kernel(const TableParams p, float4* __restrict__ table) {
+  const int j = blockIdx.x;
+  const int e = threadIdx.x;  // 16 entries
+  if (j >= p.n || e >= 16) return;
+  const int g = p.src[j];
+  const int o = e >> 2, i = e & 3;
+  auto q = [&](int x) { return p.swap[j] ? (((x & 1) << 1) | (x >> 1)) : x; };
+  const int oo = q(o), ii = q(i);
+  const int64_t* st = p.gstride[g];
+  const float2 u = p.gate[g][(oo >> 1) * st[0] + (oo & 1) * st[1] + (ii >> 1) * st[2] + (ii & 1) * st[3]];
+  table[16 * j + e] = make_float4(u.x, u.x, -u.y, u.y);
 }
 
 // Sum over the outer (non-tile) axes of tile t: one warp, lanes split the axes.
@@ -348,28 +220,23 @@ __device__ __forceinline__ int64_t tile_base(int64_t t, const int64_t* __restric
 //                      completion tracked by mbarrier full[b]), then the store
 //                      of tile k-1 (smem -> HBM in the output layout) once the
 //                      math warps released it (computed[b]), then empty[b];
-//   math warps (8):    the pass's gate groups on tensor cores, in place.
+//   math warps (8):    the pass's gate groups on 32-element register cubes.
 // Loads, math and stores of three consecutive tiles overlap.
-__global__ void __launch_bounds__(kThreads, 1) absorb_mma_kernel(const float2* __restrict__ in,
-                                                                  float2* __restrict__ out,
-                                                                  const uint32_t* __restrict__ frags,
-                                                                  const AbsorbParams p) {
-  extern __shared__ __align__(16) float2 tiles[];  // kBufs x kTile, then the pass's B fragments
+__global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* __restrict__ in,
+                                                                   float2* __restrict__ out,
+                                                                   const float4* __restrict__ table,
+                                                                   const AbsorbParams p) {
+  extern __shared__ __align__(16) float2 tiles[];  // kBufs x kTile, then the pass's gate tables
   __shared__ __align__(8) uint64_t full[kBufs], computed[kBufs], empty[kBufs];
   __shared__ int64_t s_oin[TNC_MAX_RANK], s_oout[TNC_MAX_RANK];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+  float4* su = reinterpret_cast<float4*>(tiles + kBufs * kTile);
+  for (int i = tid; i < 16 * p.n_gates; i += kThreads) su[i] = __ldg(table + 16 * p.table_base + i);
   if (tid < p.n_outer) {
     s_oin[tid] = p.outer_in[tid];
     s_oout[tid] = p.outer_out[tid];
-  }
-  // the pass's group B fragments (48 u32 per lane per group) -> smem once
-  uint32_t* sfrag = reinterpret_cast<uint32_t*>(tiles + kBufs * kTile);
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(frags + static_cast<int64_t>(p.frag_base) * 32);
-    uint4* dst = reinterpret_cast<uint4*>(sfrag);
-    for (int i = tid; i < p.n_groups * kGroupWords * 32 / 4; i += kThreads) dst[i] = __ldg(src + i);
   }
   if (tid == 0) {
     for (int b = 0; b < kBufs; ++b) {
@@ -435,7 +302,27 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_mma_kernel(const float2* _
 #pragma unroll
         for (int j = 0; j < 3; ++j)
           if ((warp >> j) & 1) base ^= gp.warp_slot[j];
-        apply_group(tile, gp, sfrag + (g * 32 + lane) * kGroupWords, base);
+        int sb[kCubeBits];
+#pragma unroll
+        for (int j = 0; j < kCubeBits; ++j) sb[j] = gp.cube_slot[j];
+        float2 c[kCube];
+#pragma unroll
+        for (int s = 0; s < kCube; ++s) {
+          int a = base;
+#pragma unroll
+          for (int j = 0; j < kCubeBits; ++j)
+            if ((s >> j) & 1) a ^= sb[j];
+          c[s] = tile[a];
+        }
+        for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], su + 16 * k2);
+#pragma unroll
+        for (int s = 0; s < kCube; ++s) {
+          int a = base;
+#pragma unroll
+          for (int j = 0; j < kCubeBits; ++j)
+            if ((s >> j) & 1) a ^= sb[j];
+          tile[a] = c[s];
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kMathThreads) : "memory");
       }
       if (tid == 0) mbar_arrive(&computed[b]);
@@ -515,19 +402,22 @@ int plan_passes(int r, const std::vector<GateRef>& gates, const std::vector<int6
     std::vector<int> rest;
     ps.gates = pack(gates, todo, ps.tile, kTB, rest);
     if (ps.gates.empty() && !todo.empty()) return set_error("absorb: a gate does not fit a tile"), TNC_ERR_UNSUPPORTED;
-    // groups of <= 4 axes (same deferral rule); groups beyond kMaxGroups go
-    // back to the remaining gates (the first k groups are a dependency-closed
-    // prefix of the pass's gates)
+    // groups of <= 5 axes (same deferral rule); groups beyond kMaxGroups
+    // (or gates beyond kMaxPassGates) go back to the remaining gates (the
+    // first k groups are a dependency-closed prefix of the pass's gates)
     {
       std::vector<int> todo2 = ps.gates;
+      int n_in = 0;
       while (!todo2.empty()) {
         std::vector<int> axes, rest2;
-        std::vector<int> grp = pack(gates, todo2, axes, 4, rest2);
-        if (static_cast<int>(ps.groups.size()) == kMaxGroups) {
+        std::vector<int> grp = pack(gates, todo2, axes, kCubeBits, rest2);
+        if (static_cast<int>(ps.groups.size()) == kMaxGroups ||
+            n_in + static_cast<int>(grp.size()) > kMaxPassGates) {
           rest.insert(rest.end(), todo2.begin(), todo2.end());
           std::sort(rest.begin(), rest.end());
           break;
         }
+        n_in += static_cast<int>(grp.size());
         ps.groups.push_back(grp);
         ps.gaxes.push_back(axes);
         todo2 = rest2;
@@ -642,9 +532,10 @@ std::vector<int> place_bits(const std::vector<int>& tile, const std::vector<int6
   return bit_axis;  // bit position -> physical axis
 }
 
-int build_pass_params(int r, const Pass& ps, const std::vector<int>& bit_axis, const std::vector<int64_t>& in_st,
-                      const std::vector<int64_t>& out_st, int frag_base /* u32 x 32 units */, AbsorbParams& p,
-                      std::vector<std::vector<int>>& group_colbits) {
+// group_local: (chain gate index, swap) of the pass's gates in table order
+int build_pass_params(int r, const Pass& ps, const std::vector<GateRef>& gates_of_pass, const std::vector<int>& bit_axis,
+                      const std::vector<int64_t>& in_st, const std::vector<int64_t>& out_st, int table_base,
+                      AbsorbParams& p, std::vector<std::pair<int, int>>& group_local) {
   std::memset(&p, 0, sizeof(p));
   std::vector<int> pos(r, -1);
   for (int b = 0; b < kTB; ++b) pos[bit_axis[b]] = b;
@@ -692,76 +583,54 @@ int build_pass_params(int r, const Pass& ps, const std::vector<int>& bit_axis, c
   }
   p.n_tiles = static_cast<int64_t>(1) << p.n_outer;
   p.n_groups = static_cast<int>(ps.groups.size());
-  group_colbits.clear();
-  int foff = frag_base;
-  p.frag_base = frag_base;
+  p.table_base = table_base;
+  // each group: 5 cube bits (its axes + padding), 5 lane bits (the first 4
+  // of distinct bank classes), 3 warp bits; gates oriented so in_a is the
+  // lower cube bit
+  group_local.clear();
+  p.n_gates = 0;
   for (int g = 0; g < p.n_groups; ++g) {
-    std::vector<int> gb;  // tile bits of the group's axes
-    for (int a : ps.gaxes[g]) gb.push_back(pos[a]);
     auto cl = [](int b) { return b & 3; };
-    const int w = 4;
-    // pad a smaller group to 4 column bits with row bits of fresh classes
-    while (static_cast<int>(gb.size()) < w) {
-      int best = -1;
-      for (int b = 0; b < kTB && best < 0; ++b) {
-        bool fresh = !has(gb, b);
-        for (int x : gb) fresh = fresh && cl(x) != cl(b);
-        if (fresh) best = b;
-      }
-      for (int b = 0; b < kTB && best < 0; ++b)
-        if (!has(gb, b)) best = b;
-      gb.push_back(best);
-    }
-    // q0, q1 (lane bits 0, 1): two column bits of distinct classes
-    std::vector<int> cols = gb;
-    for (size_t i = 0; i < cols.size(); ++i)
-      for (size_t j = i + 1; j < cols.size(); ++j)
-        if (cl(cols[i]) != cl(cols[j]) && !(i == 0 && j == 1) && cl(cols[0]) == cl(cols[1])) {
-          std::swap(cols[0], cols[i]);
-          std::swap(cols[1], cols[j]);
-        }
-    std::vector<int> rows;
+    std::vector<int> cube;
+    for (int a : ps.gaxes[g]) cube.push_back(pos[a]);
+    std::vector<int> rest_bits;
     for (int b = 0; b < kTB; ++b)
-      if (!has(cols, b)) rows.push_back(b);
-    // g0, g1: row bits completing the 4 classes of a half-warp
-    std::vector<int> lane_bits = {cols[0], cols[1]};
-    for (int pass_ = 0; pass_ < 2; ++pass_) {
-      for (int b : rows) {
-        if (static_cast<int>(lane_bits.size()) >= 4) break;
-        if (has(lane_bits, b)) continue;
-        bool distinct = true;
-        for (int x : lane_bits) distinct = distinct && cl(x) != cl(b);
-        if (distinct || pass_ == 1) lane_bits.push_back(b);
-      }
-    }
-    std::vector<int> others;
-    for (int b : rows)
-      if (!has(lane_bits, b)) others.push_back(b);
-    // others (7 bits): g2, h, warp x3, iteration x2
+      if (!has(cube, b)) rest_bits.push_back(b);
+    // lane bits 0..3 of distinct classes from the non-cube bits, chosen first so
+    // the padding cube bits do not take them
+    std::vector<int> lanes;
+    for (int c = 0; c < 4; ++c)
+      for (int b : rest_bits)
+        if (cl(b) == c && !has(lanes, b)) {
+          lanes.push_back(b);
+          break;
+        }
+    std::vector<int> free_bits;
+    for (int b : rest_bits)
+      if (!has(lanes, b)) free_bits.push_back(b);
+    size_t fi = 0;
+    while (static_cast<int>(cube.size()) < kCubeBits) cube.push_back(free_bits[fi++]);
+    while (lanes.size() < 5) lanes.push_back(free_bits[fi++]);
+    std::vector<int> warps(free_bits.begin() + fi, free_bits.end());
     GroupParams& gp = p.g[g];
-    gp.frag_off = foff;
-    foff += kGroupWords;
-    for (int j = 0; j < 4; ++j) gp.lane_slot[j] = swz(1 << lane_bits[j]);
-    gp.lane_slot[4] = swz(1 << others[0]);
-    gp.h_slot = swz(1 << others[1]);
-    for (int j = 0; j < 3; ++j) gp.warp_slot[j] = swz(1 << others[2 + j]);
-    for (int m = 0; m < 4; ++m) {
-      int x = 0;
-      for (int j = 0; j < 2; ++j)
-        if ((m >> j) & 1) x ^= swz(1 << others[5 + j]);
-      gp.iter[m] = x;
+    for (int j = 0; j < kCubeBits; ++j) gp.cube_slot[j] = swz(1 << cube[j]);
+    for (int j = 0; j < 5; ++j) gp.lane_slot[j] = swz(1 << lanes[j]);
+    for (int j = 0; j < 3; ++j) gp.warp_slot[j] = swz(1 << warps[j]);
+    gp.g_first = p.n_gates;
+    for (int gi : ps.groups[g]) {
+      auto ci = [&](int axis) {
+        return static_cast<int>(std::find(cube.begin(), cube.end(), pos[axis]) - cube.begin());
+      };
+      int la = ci(gates_of_pass[gi].pa), lb = ci(gates_of_pass[gi].pb);
+      const bool swap = la > lb;
+      if (swap) std::swap(la, lb);
+      p.gate_local[p.n_gates++] = 8 * la + lb;
+      group_local.push_back({gi, swap ? 1 : 0});
     }
-    gp.q2_slot = swz(1 << cols[2]);
-    gp.q3_slot = swz(1 << cols[3]);
-    // column bit c of the group unitary <-> tile bit cols[c]
-    group_colbits.push_back(cols);
-    if (std::getenv("TNC_ABSORB_DEBUG")) {
-      auto cl = [](int b) { return b & 3; };
-      std::fprintf(stderr, "  group %d: gates %zu axes %zu cols [%d %d %d %d] lanes [%d %d %d %d] classes [%d %d %d %d]\n", g,
-                   ps.groups[g].size(), ps.gaxes[g].size(), cols[0], cols[1], cols[2], cols[3], lane_bits[0],
-                   lane_bits[1], lane_bits[2], lane_bits[3], cl(lane_bits[0]), cl(lane_bits[1]), cl(lane_bits[2]),
-                   cl(lane_bits[3]));
-    }
+    gp.g_last = p.n_gates;
+    if (std::getenv("TNC_ABSORB_DEBUG"))
+      std::fprintf(stderr, "  group %d: %zu gates, %zu axes, lane classes %d %d %d %d\n", g, ps.groups[g].size(),
+                   ps.gaxes[g].size(), cl(lanes[0]), cl(lanes[1]), cl(lanes[2]), cl(lanes[3]));
   }
   return TNC_OK;
 }
@@ -823,14 +692,11 @@ int plan_chain(int r, int n_gates, const int32_t* axes, ChainPlan& cp) {
   }
   cp.total_groups = 0;
   for (auto& ps : cp.passes) cp.total_groups += static_cast<int>(ps.groups.size());
-  if (cp.total_groups > kMaxAllGroups) TNC_RET(TNC_ERR_UNSUPPORTED, "absorb: too many gate groups");
   return TNC_OK;
 }
 
-// fragment table: 32 u32 per lane per group
-size_t frag_bytes(const ChainPlan& cp) {
-  return (std::max<size_t>(static_cast<size_t>(cp.total_groups) * kGroupWords * 32, 1) * 4 + 255) & ~size_t(255);
-}
+// gate tables: 16 float4 per gate
+size_t table_bytes(int n_gates) { return (static_cast<size_t>(std::max(n_gates, 1)) * 256 + 255) & ~size_t(255); }
 
 }  // namespace
 
@@ -838,7 +704,7 @@ int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t*
   ChainPlan cp;
   TNC_TRY(plan_chain(t_rank, n_gates, axes, cp));
   const size_t tensor = cp.passes.size() > 1 ? (static_cast<size_t>(1) << t_rank) * sizeof(float2) : 0;
-  *bytes = tensor + frag_bytes(cp);
+  *bytes = tensor + table_bytes(n_gates);
   return TNC_OK;
 }
 
@@ -850,61 +716,41 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
   TNC_TRY(plan_chain(r, n_gates, axes, cp));
   const int P = static_cast<int>(cp.passes.size());
   const size_t tensor = P > 1 ? (static_cast<size_t>(1) << r) * sizeof(float2) : 0;
-  if (workspace_bytes < tensor + frag_bytes(cp) || workspace == nullptr)
+  if (workspace_bytes < tensor + table_bytes(n_gates) || workspace == nullptr)
     TNC_RET(TNC_ERR_WORKSPACE, "absorb: workspace too small (see tnc_absorb_chain_workspace)");
   for (int g = 0; g < n_gates; ++g)
     if (gates[g] == nullptr) TNC_RET(TNC_ERR_INVALID, "absorb: null gate pointer");
   float2* ws = static_cast<float2*>(workspace);
-  uint32_t* table = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + tensor);
+  float4* table = reinterpret_cast<float4*>(static_cast<uint8_t*>(workspace) + tensor);
 
-  // per-pass parameters (bit placement needs both layouts)
   std::vector<AbsorbParams> params(P);
-  FragParams fp;
-  std::memset(&fp, 0, sizeof(fp));
-  int gbase = 0, gidx = 0, foff = 0;
+  TableParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  int base = 0;
   for (int k = 0; k < P; ++k) {
     const Pass& ps = cp.passes[k];
-    const std::vector<int> bit_axis = place_bits(ps.tile, cp.in_st[k], cp.out_st[k]);
-    std::vector<std::vector<int>> colbits;
-    TNC_TRY(build_pass_params(r, ps, bit_axis, cp.in_st[k], cp.out_st[k], foff, params[k], colbits));
-    std::vector<int> pos(r, -1);
-    for (int b = 0; b < kTB; ++b) pos[bit_axis[b]] = b;
-    for (size_t g = 0; g < ps.groups.size(); ++g) {
-      fp.grp_first[gbase + g] = gidx;
-      fp.grp_off[gbase + g] = params[k].g[g].frag_off;
-      fp.grp_w[gbase + g] = static_cast<signed char>(colbits[g].size());
-      foff += kGroupWords;
-      for (int gi : ps.groups[g]) {
-        const GateRef& gr = cp.refs[gi];
-        auto col = [&](int axis) {
-          const int b = pos[axis];
-          for (size_t c = 0; c < colbits[g].size(); ++c)
-            if (colbits[g][c] == b) return static_cast<int>(c);
-          return -1;
-        };
-        fp.grp_gate[gidx] = static_cast<short>(gi);
-        fp.grp_ca[gidx] = static_cast<signed char>(col(gr.pa));
-        fp.grp_cb[gidx] = static_cast<signed char>(col(gr.pb));
-        ++gidx;
-      }
+    std::vector<std::pair<int, int>> gl;
+    TNC_TRY(build_pass_params(r, ps, cp.refs, place_bits(ps.tile, cp.in_st[k], cp.out_st[k]), cp.in_st[k],
+                              cp.out_st[k], base, params[k], gl));
+    for (const auto& e : gl) {
+      tp.src[base] = static_cast<short>(e.first);
+      tp.swap[base] = static_cast<signed char>(e.second);
+      ++base;
     }
-    gbase += static_cast<int>(ps.groups.size());
   }
-  fp.grp_first[gbase] = gidx;
-  fp.n_groups = gbase;
+  tp.n = base;
   for (int g = 0; g < n_gates; ++g) {
-    fp.gate[g] = static_cast<const float2*>(gates[g]);
-    for (int k = 0; k < 4; ++k) fp.gstride[g][k] = gate_strides[4 * g + k];
+    tp.gate[g] = static_cast<const float2*>(gates[g]);
+    for (int k = 0; k < 4; ++k) tp.gstride[g][k] = gate_strides[4 * g + k];
   }
-  if (fp.n_groups > 0) {
-    absorb_frag_kernel<<<fp.n_groups, 32, 0, stream>>>(fp, table);
+  if (tp.n > 0) {
+    absorb_table_kernel<<<tp.n, 16, 0, stream>>>(tp, table);
     TNC_CHECK_LAUNCH();
   }
-  int max_groups = 0;
-  for (const auto& prm : params) max_groups = std::max(max_groups, prm.n_groups);
-  const size_t smem = static_cast<size_t>(kBufs) * kTile * sizeof(float2) +
-                      static_cast<size_t>(max_groups) * kGroupWords * 32 * 4;
-  TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  int max_gates = 0;
+  for (const auto& prm : params) max_gates = std::max(max_gates, prm.n_gates);
+  const size_t smem = static_cast<size_t>(kBufs) * kTile * sizeof(float2) + static_cast<size_t>(max_gates) * 256;
+  TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
   const float2* cur = static_cast<const float2*>(t_in);
   for (int k = 0; k < P; ++k) {
@@ -912,9 +758,10 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
     const AbsorbParams& p = params[k];
     const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()));
     {
-      ProfScope prof(PROF_ABSORB, 768.0 * p.n_groups * static_cast<double>(int64_t(1) << r),
+      // algorithmic work: 16 complex MACs (64 real flops) per 4 elements per gate
+      ProfScope prof(PROF_ABSORB, 32.0 * p.n_gates * static_cast<double>(int64_t(1) << r),
                      16.0 * static_cast<double>(int64_t(1) << r), stream);
-      absorb_mma_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(cur, dst, table, p);
+      absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(cur, dst, table, p);
       TNC_CHECK_LAUNCH();
     }
     cur = dst;
@@ -930,9 +777,9 @@ int absorb_chain_passes(int t_rank, int n_gates, const int32_t* axes, int* passe
   if (std::getenv("TNC_ABSORB_DEBUG")) {  // print the bit placement of every pass
     AbsorbParams* prm = new AbsorbParams;
     for (size_t k = 0; k < cp.passes.size(); ++k) {
-      std::vector<std::vector<int>> colbits;
-      build_pass_params(t_rank, cp.passes[k], place_bits(cp.passes[k].tile, cp.in_st[k], cp.out_st[k]), cp.in_st[k],
-                        cp.out_st[k], 0, *prm, colbits);
+      std::vector<std::pair<int, int>> gl;
+      build_pass_params(t_rank, cp.passes[k], cp.refs, place_bits(cp.passes[k].tile, cp.in_st[k], cp.out_st[k]),
+                        cp.in_st[k], cp.out_st[k], 0, *prm, gl);
     }
     delete prm;
   }
