@@ -24,8 +24,12 @@
  *    contiguous (last leg fastest), exactly the reference layout
  *    (tensor.py:3-9).  Arbitrary strides allow zero-copy projected views.
  *  - The caller owns every device buffer (inputs, outputs, workspace); the
- *    library never allocates per call.  All launches are asynchronous on
- *    the caller's stream (a cudaStream_t passed as void*); no implicit sync.
+ *    per-call entry points (tnc_contract, tnc_contract_split, tnc_permute,
+ *    tnc_absorb_chain, tnc_axpy) never allocate and never synchronise: all
+ *    launches are asynchronous on the caller's stream (a cudaStream_t passed
+ *    as void*), so they can be captured in a CUDA graph.  tnc_plan_contract
+ *    may allocate the plan's device index tables (uploaded and synchronised
+ *    once, at plan creation); tnc_plan_destroy frees them.
  *  - Plans are immutable and may be shared across threads.
  *  - Return values are tnc_status codes; tnc_last_error() returns a
  *    thread-local message for the last failure on the calling thread.
@@ -104,6 +108,9 @@ typedef struct tnc_plan_info {
 /* ---- library / device ---------------------------------------------------- */
 int tnc_abi_version(void);
 int tnc_init(int device);
+/* Release process-wide library state (profiling events).  Plans own their
+ * device tables and free them in tnc_plan_destroy.  Idempotent. */
+void tnc_shutdown(void);
 const char* tnc_last_error(void);
 int tnc_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* smem_optin);
 

@@ -8,7 +8,7 @@ travel instead.
 
     python oracle/gen_golden.py [section ...]
 
-Sections: perm contract split c0 plans sliced reuse pairs spill plan_c4_reuse
+Sections: perm contract split c0 plans sliced reuse pairs spill plan_c4_reuse split_order
 """
 
 from __future__ import annotations
@@ -176,6 +176,26 @@ def section_split():
     out.append({"a": [["a", 2], ["k", 3], ["m", 2]], "b": [["k", 3], ["m", 2], ["b", 2]], "a_data": _c(da),
                 "b_data": _c(db), "blocks": 4, "group": 1, "out_labels": list(res.labels), "out": _c(res.data)})
     _dump("split", {"cases": out})
+
+
+def section_split_order():
+    """split_common_contract when B is the larger operand and lists the common
+    legs in a different order than A: the reference cuts K into panels in A's
+    common order (contract.py:58-75,168-208).  Values are chosen so that the
+    complex128 result depends on the panel boundaries (1e16 + 1 rounds away in
+    one partition, not in the other)."""
+    ia = [RIndex("k0"), RIndex("k1")]
+    ib = [RIndex("k1"), RIndex("k0"), RIndex("b0")]
+    da = np.array([1e16, 1.0, -1e16, 0.0], dtype=np.complex128)  # A[k0][k1]
+    db = np.ones(8, dtype=np.complex128)
+    a = tncsim.DenseTensor(ia, da, precision="double")
+    b = tncsim.DenseTensor(ib, db, precision="double")
+    cases = []
+    for bl, gr in ((2, 1), (4, 1), (1, 1)):
+        res = tncsim.split_common_contract(a, b, bl, gr)
+        cases.append({"blocks": bl, "group": gr, "out_labels": list(res.labels), "out": _c(res.data)})
+    _dump("split_order", {"a": ["k0", "k1"], "b": ["k1", "k0", "b0"], "a_data": _c(da), "b_data": _c(db),
+                          "cases": cases})
 
 
 def _steps(s):
@@ -418,6 +438,7 @@ SECTIONS = {
     "perm": section_perm, "contract": section_contract, "split": section_split, "c0": section_c0,
     "plans": section_plans, "sliced": section_sliced, "reuse": section_reuse, "pairs": section_pairs,
     "spill": section_spill, "plan_c4_reuse": section_plan_c4_reuse,
+    "split_order": section_split_order,
 }
 
 if __name__ == "__main__":

@@ -57,6 +57,7 @@ _SZ = ctypes.c_size_t
 SIGNATURES = {
     "tnc_abi_version": (ctypes.c_int, []),
     "tnc_init": (ctypes.c_int, [ctypes.c_int]),
+    "tnc_shutdown": (None, []),
     "tnc_last_error": (ctypes.c_char_p, []),
     "tnc_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_SZ)]),

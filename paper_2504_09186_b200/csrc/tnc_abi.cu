@@ -98,6 +98,11 @@ struct tnc_plan {
   int64_t kp;             // padded K for the tensor-core planes
   int32_t n_common;
   tnc::Operand x, y;
+  // split_common_contract panels cut K in A's common order (reference
+  // contract.py:58-75, 168-208); when B is the row side, x / y list the
+  // commons in B's order (in-place friendly), so the split path uses these
+  tnc::Operand sx, sy;
+  bool split_alt = false;
   int64_t ldcm, ldcn;      // C[x, y] strides in the (default-order) result
   bool custom_out;         // result order is a different permutation
   std::vector<int64_t> out_perm_dims, out_perm_strides;
@@ -120,7 +125,6 @@ struct tnc_plan {
   int32_t g_x_kfast = 1, g_y_kfast = 1;
   int64_t g_chunks = 1;
   std::vector<int64_t> g_host;
-  mutable std::mutex g_mu;
   mutable int64_t* g_dev = nullptr;
   ~tnc_plan() {
     if (g_dev) cudaFree(g_dev);
@@ -269,6 +273,7 @@ bool build_gather_splitk(tnc_plan* p) {
   int64_t kc = ceil_div(p->k, target);
   kc = std::max<int64_t>(64, ceil_div(kc, 64) * 64);
   p->g_chunks = ceil_div(p->k, kc);
+  if (upload_table(p->g_host.data(), p->g_host.size(), &p->g_dev) != TNC_OK) return false;
   p->gather_splitk = true;
   return true;
 }
@@ -434,6 +439,14 @@ int tnc_init(int device) {
   return TNC_OK;
 }
 
+// Releases the library's process-wide state (profiling events); device
+// buffers owned by plans are released by tnc_plan_destroy.  Safe to call
+// more than once; the library stays usable (tnc_init again).
+void tnc_shutdown(void) {
+  tnc_profile_enable(0);
+  cudaGetLastError();  // clear a sticky launch error from a failed call
+}
+
 int tnc_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* smem_optin) {
   int dev = 0;
   TNC_CUDA_TRY(cudaGetDevice(&dev));
@@ -526,6 +539,23 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
   }
   p->rows_x = p->x_is_a ? m : n;
   p->rows_y = p->x_is_a ? n : m;
+  if (!p->x_is_a && common_a.size() > 1) {
+    p->split_alt = true;
+    p->sx.free = free_b;
+    p->sy.free = free_a;
+    p->sx.common = common_b;  // listed in A's common order
+    p->sy.common = common_a;
+    for (Operand* op : {&p->sx, &p->sy}) {
+      int64_t rows = 1;
+      for (auto& l : op->free) rows *= l.dim;
+      op->rows = rows;
+      op->in_place = matrix_view(op->free, op->common, &op->ld);
+      if (!op->in_place) {
+        build_gather(*op);
+        op->ld = k;
+      }
+    }
+  }
   for (Operand* op : {&X, &Y}) {
     int64_t rows = 1;
     for (auto& l : op->free) rows *= l.dim;
@@ -791,14 +821,7 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
                            reinterpret_cast<float*>(ws + p->off_partials), st);
   }
   if (p->variant == TNC_VARIANT_SPLITK && p->gather_splitk) {
-    {
-      std::lock_guard<std::mutex> lk(p->g_mu);
-      if (!p->g_dev) {
-        const size_t bytes = p->g_host.size() * sizeof(int64_t);
-        TNC_CUDA_TRY(cudaMalloc(&p->g_dev, bytes));
-        TNC_CUDA_TRY(cudaMemcpy(p->g_dev, p->g_host.data(), bytes, cudaMemcpyHostToDevice));
-      }
-    }
+    if (!p->g_dev) TNC_RET(TNC_ERR_INVALID, "split-K gather: plan tables missing");
     return splitk_gather_launch(p->dtype, p->rows_x, p->rows_y, p->k, xm, ym, p->g_dev, p->g_size,
                                 p->g_x_kfast, p->g_y_kfast, p->g_chunks, c, ldcm, ldcn,
                                 ws + p->off_partials, st);
@@ -883,8 +906,11 @@ int tnc_contract_split(const tnc_plan* p, int32_t blocks, int32_t group, const v
   const void* ysrc = p->x_is_a ? b : a;
   const void *xm, *ym;
   int64_t ldx, ldy;
-  TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
-  TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
+  // operands staged after the panel partials (K in A's common order)
+  const size_t off_sx = align_up(p->ws_layout) + align_up(static_cast<size_t>(panels) * p->m * p->n * eb);
+  const size_t off_sy = off_sx + align_up(static_cast<size_t>(p->rows_x) * p->k * eb);
+  TNC_TRY(prep_operand(p, p->split_alt ? p->sx : p->x, xsrc, ws, off_sx, &xm, &ldx, st));
+  TNC_TRY(prep_operand(p, p->split_alt ? p->sy : p->y, ysrc, ws, off_sy, &ym, &ldy, st));
   const int64_t mn = p->m * p->n;
   // each panel accumulates independently into its own [rows_x, rows_y] tile
   for (int64_t i = 0; i < panels; ++i) {

@@ -93,6 +93,20 @@ inline int num_sms() {
 
 inline size_t elem_bytes(int dtype) { return dtype == TNC_C128 ? 16 : 8; }
 
+// Plan-time upload of a host index table to a device buffer owned by the plan
+// (freed with the plan).  Plan creation may allocate and synchronise; the
+// per-call launch paths (tnc_contract) never do.  The pageable copy is
+// completed (legacy-stream sync) before returning, so kernels on any stream
+// see the table.
+inline int upload_table(const int64_t* host, size_t n, int64_t** dev) {
+  *dev = nullptr;
+  if (n == 0) return TNC_OK;
+  TNC_CUDA_TRY(cudaMalloc(dev, n * sizeof(int64_t)));
+  TNC_CUDA_TRY(cudaMemcpy(*dev, host, n * sizeof(int64_t), cudaMemcpyHostToDevice));
+  TNC_CUDA_TRY(cudaStreamSynchronize(cudaStreamLegacy));
+  return TNC_OK;
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Compact description of a strided n-d view used by the gather kernels.

@@ -550,7 +550,6 @@ struct GatherTcPlan {
   int nmma = 0, kbc = 0;
   int64_t rows_x = 0, rows_y = 0, k = 0;
   std::vector<int64_t> tabs_host;
-  mutable std::mutex mu;
   mutable int64_t* tabs_dev = nullptr;
   ~GatherTcPlan() {
     if (tabs_dev) cudaFree(tabs_dev);
@@ -961,6 +960,11 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
       plan->pair_y = py;
     }
   }
+  const int up = upload_table(plan->tabs_host.data(), plan->tabs_host.size(), &plan->tabs_dev);
+  if (up != TNC_OK) {
+    delete plan;
+    return up;
+  }
   *out = plan;
   return TNC_OK;
 }
@@ -987,14 +991,7 @@ int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cuda
 
 int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, void* c_final, void* parts,
                      cudaStream_t stream) {
-  {
-    std::lock_guard<std::mutex> lk(plan->mu);
-    if (!plan->tabs_dev) {
-      const size_t bytes = plan->tabs_host.size() * sizeof(int64_t);
-      TNC_CUDA_TRY(cudaMalloc(&plan->tabs_dev, bytes));
-      TNC_CUDA_TRY(cudaMemcpy(plan->tabs_dev, plan->tabs_host.data(), bytes, cudaMemcpyHostToDevice));
-    }
-  }
+  if (!plan->tabs_dev && !plan->tabs_host.empty()) TNC_RET(TNC_ERR_INVALID, "tc_gather: plan tables missing");
   // paired layout when the plan has one and the operands are 16-byte aligned
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                        (!plan->pair_y || (reinterpret_cast<uintptr_t>(y) & 15) == 0);

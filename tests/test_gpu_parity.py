@@ -190,6 +190,24 @@ def test_split_common_golden(cuda_ready):
         assert rel_l2(got.numpy(), arr(case["out"])) <= TOL_C64
 
 
+def test_split_panels_follow_a_common_order(cuda_ready):
+    """split_common_contract with B larger and its common legs permuted
+    relative to A: the panels cut K in A's common order, so the
+    cancellation-sensitive complex128 result equals the reference's bit for bit
+    (advisor finding: B-order panels gave 1 instead of 0)."""
+    from paper_2504_09186_b200 import DenseTensor, split_common_contract
+
+    g = load_golden("split_order")
+    a = DenseTensor(_idx([(l, 2) for l in g["a"]]), arr(g["a_data"]), precision="double")
+    b = DenseTensor(_idx([(l, 2) for l in g["b"]]), arr(g["b_data"]), precision="double")
+    for case in g["cases"]:
+        if case["blocks"] == 1:
+            continue
+        got = split_common_contract(a, b, case["blocks"], case["group"])
+        assert [ix.label for ix in got.indices] == case["out_labels"]
+        assert np.array_equal(got.numpy(), arr(case["out"])), (case["blocks"], got.numpy())
+
+
 def test_split_degenerate_equals_pair_bitwise(cuda_ready):
     from paper_2504_09186_b200 import DenseTensor, Index, contract_pair, split_common_contract
 
