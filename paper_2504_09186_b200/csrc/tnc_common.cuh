@@ -98,9 +98,16 @@ inline size_t elem_bytes(int dtype) { return dtype == TNC_C128 ? 16 : 8; }
 // per-call launch paths (tnc_contract) never do.  The pageable copy is
 // completed (legacy-stream sync) before returning, so kernels on any stream
 // see the table.
+// Host-only processes (no CUDA device) still plan: the table stays pending
+// and a launch of such a plan reports an error.
 inline int upload_table(const int64_t* host, size_t n, int64_t** dev) {
   *dev = nullptr;
   if (n == 0) return TNC_OK;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return TNC_OK;
+  }
   TNC_CUDA_TRY(cudaMalloc(dev, n * sizeof(int64_t)));
   TNC_CUDA_TRY(cudaMemcpy(*dev, host, n * sizeof(int64_t), cudaMemcpyHostToDevice));
   TNC_CUDA_TRY(cudaStreamSynchronize(cudaStreamLegacy));
