@@ -142,27 +142,41 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def measure_tf32_peak() -> dict:
+def measure_tf32_peak(sustain_s: float = 2.0) -> dict:
     """cuBLAS TF32 GEMM throughput on this GPU (MEASURED_PEAKS.json has no
-    TF32 entry): fp32 8192^3 matmul with TF32 enabled, best of 10 (burst)."""
+    TF32 entry): fp32 8192^3 matmul with TF32 enabled -- best of 10 (burst)
+    and back to back for ``sustain_s`` seconds (sustained), mirroring the
+    driver's bf16 measurement."""
     import torch
 
+    prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = True
     n = 8192
     a = torch.randn(n, n, device="cuda")
     b = torch.randn(n, n, device="cuda")
+    c = torch.empty(n, n, device="cuda")
     for _ in range(3):
-        a @ b
+        torch.matmul(a, b, out=c)
     best = float("inf")
     for _ in range(10):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        a @ b
+        torch.matmul(a, b, out=c)
         e.record()
         e.synchronize()
         best = min(best, s.elapsed_time(e) / 1e3)
-    torch.backends.cuda.matmul.allow_tf32 = False
-    return {"tf32_tflops": 2 * n ** 3 / best / 1e12, "how": "torch fp32 matmul 8192^3, allow_tf32, best of 10"}
+    reps = max(1, int(sustain_s / best))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        torch.matmul(a, b, out=c)
+    e.record()
+    e.synchronize()
+    sustained = 2 * n ** 3 * reps / (s.elapsed_time(e) / 1e3) / 1e12
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    del a, b, c
+    return {"tf32_tflops": 2 * n ** 3 / best / 1e12, "tf32_tflops_sustained": sustained,
+            "how": f"torch fp32 matmul 8192^3 with allow_tf32: best of 10 (burst), {reps} back to back (sustained)"}
 
 
 def measured_peaks() -> dict:
@@ -382,12 +396,12 @@ def bench_c3(args) -> None:
 
     if rank == 0:
         peaks = measured_peaks()
+        tf32 = measure_tf32_peak()
         if os.environ.get("TNC_TC_TF32", "0") not in ("", "0"):
-            tf32 = measure_tf32_peak()
-            p_eff = tf32["tf32_tflops"] / 3.0
+            p_eff = tf32["tf32_tflops_sustained"] / 3.0
             kernel_name = "tc_cgemm_kernel<.., F16=false> (3xTF32 tcgen05.mma kind::tf32)"
-            peak_source = (f"measured cuBLAS TF32 {tf32['tf32_tflops']:.0f} TF/s (burst) / 3 products; "
-                           "MEASURED_PEAKS.json has no TF32 entry")
+            peak_source = (f"measured cuBLAS TF32 {tf32['tf32_tflops_sustained']:.0f} TF/s (sustained, this run) "
+                           "/ 3 products; MEASURED_PEAKS.json has no TF32 entry")
             dtype = "c64 (3xTF32 tensor-core GEMM, fp32 accumulate)"
         else:
             # 3xFP16: three fp16 tensor-core products per complex-GEMM flop pair;
@@ -398,6 +412,7 @@ def bench_c3(args) -> None:
                            "TF/s (fp16 rate) / 3 products")
             dtype = "c64 (3xFP16 tensor-core GEMM, fp32 accumulate)"
         tc = prof["tc_gemm"]
+        traffic_bytes, traffic_detail = _profiled_traffic(args.workload)
         achieved = tc["flops"] / (tc["ms"] / 1e3) / 1e12 if tc["ms"] > 0 else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -429,14 +444,15 @@ def bench_c3(args) -> None:
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_eff, "unit": "TFLOP/s",
                          "frac": (achieved / p_eff) if achieved else None,
-                         "traffic": _profiled_traffic(args.workload),
-                         "traffic_source": "profiles/r01_tc_traffic.json (ncu dram__bytes_read+write per "
-                                           "tc_cgemm launch, C3 slice)" if args.workload == "c3" else None,
+                         "traffic": traffic_bytes,
+                         "traffic_detail": traffic_detail,
                          "kernel": kernel_name, "peak_source": peak_source,
                          "launches": tc["launches"], "share_of_step": tc["ms"] / 1e3 / elapsed},
             "kernels": prof, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
             "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops"),
-                      "bf16_tflops_sustained": peaks.get("bf16_tflops_sustained")},
+                      "bf16_tflops_sustained": peaks.get("bf16_tflops_sustained"),
+                      "tf32_measured_this_run": tf32,
+                      "p_eff_3xtf32_tflops": tf32["tf32_tflops_sustained"] / 3.0},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -616,13 +632,26 @@ def bench_c1(args) -> None:
 
 
 def _profiled_traffic(workload: str):
-    """DRAM bytes per tensor-core GEMM launch from the committed ncu capture of
-    this same command (profiles/r01_tc_traffic.json); None when not captured."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_tc_traffic.json")
-    if workload != "c3" or not os.path.exists(path):
-        return None
-    with open(path) as f:
-        return json.load(f).get("dram_bytes_per_launch")
+    """DRAM bytes of the dominant tensor-core GEMM launch (the (15,15,14) C3
+    step) from the latest committed ncu capture of this command
+    (profiles/rNN_tc_traffic.json), with its own algorithmic bytes; None when
+    not captured."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          "r*_tc_traffic.json")))
+    if workload != "c3" or not paths:
+        return None, None
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    dom = d.get("dominant")
+    if dom is None:  # round-1 format: launches only
+        launch = max(d["launches"], key=lambda x: x.get("gpu__time_duration.sum", 0))
+        dom = {"dram_bytes": launch["dram__bytes_read.sum"] + launch["dram__bytes_write.sum"],
+               "algorithmic_bytes_c64": 8 * (2 ** 30 + 2 ** 29 + 2 ** 29)}
+        dom["traffic_over_algorithmic"] = dom["dram_bytes"] / dom["algorithmic_bytes_c64"]
+    return dom["dram_bytes"], {"source": os.path.relpath(paths[-1], os.path.dirname(os.path.abspath(__file__))),
+                               "dominant_launch": dom}
 
 
 def _read_prof(lib) -> dict:
@@ -647,7 +676,7 @@ def main() -> None:
     ap.add_argument("--slices-per-step", type=int, default=1)
     ap.add_argument("--variant", type=int, default=0, help="c1: force a kernel variant (tnc_variant)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-cap", type=int, default=26)
+    ap.add_argument("--cpu-cap", type=int, default=25)
     ap.add_argument("--ref-cap", type=int, default=25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reuse", type=int, default=0,

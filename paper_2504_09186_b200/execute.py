@@ -182,6 +182,60 @@ def _leaves_at(tensors: Sequence[DenseTensor], precision: str) -> list[DenseTens
     return out
 
 
+MIN_ABSORB_RUN = 2  # gates per fused run (a single gate stays a plain step)
+
+
+def absorb_runs(s: LinearSchedule, sliced: frozenset = frozenset(), positions=None) -> dict[int, list[int]]:
+    """Stem chains the fused absorb kernel (K4) can take: maximal runs of
+    consecutive schedule positions where each step contracts the previous
+    step's result (as ``lhs``, so the reference order free_T ++ free_G holds)
+    with a leaf gate (``rhs``: rank 4, extent-2 legs, no sliced leg, sharing
+    exactly two legs with the running tensor), and the running tensor has
+    rank >= 13 (after projecting the sliced labels).  These are the
+    absorption chains of reference ``tree.py:278-330`` (``_detect_stems``) in
+    the order ``linearize`` keeps them.  ``positions`` restricts the runs to
+    the steps a caller executes.  Returns {first position: [positions]}."""
+    from .fusion import MIN_FUSED_RANK
+
+    allowed = set(range(len(s.steps))) if positions is None else set(positions)
+
+    def rank(ref):
+        return sum(1 for ix in s.indices_of(ref) if ix.label not in sliced)
+
+    def gate_ok(pos, run_ref):
+        st = s.steps[pos]
+        if pos not in allowed or st.lhs != run_ref or st.rhs >= s.n_leaves:
+            return False
+        g = s.indices_of(st.rhs)
+        if len(g) != 4 or any(ix.dim != 2 or ix.label in sliced for ix in g):
+            return False
+        t = {ix.label for ix in s.indices_of(st.lhs) if ix.label not in sliced}
+        if sum(1 for ix in g if ix.label in t) != 2:
+            return False
+        return all(ix.dim == 2 for ix in s.indices_of(st.lhs)) and rank(st.lhs) >= MIN_FUSED_RANK
+
+    runs: dict[int, list[int]] = {}
+    pos = 0
+    while pos < len(s.steps):
+        st = s.steps[pos]
+        if gate_ok(pos, st.lhs):
+            run = [pos]
+            while run[-1] + 1 < len(s.steps) and gate_ok(run[-1] + 1, s.steps[run[-1]].result):
+                run.append(run[-1] + 1)
+            if len(run) >= MIN_ABSORB_RUN:
+                runs[pos] = run
+            pos = run[-1] + 1
+        else:
+            pos += 1
+    return runs
+
+
+def _fuse_enabled() -> bool:
+    import os
+
+    return os.environ.get("TNC_FUSE_ABSORB", "1") not in ("0", "")
+
+
 class Engine:
     """Per-run device state: leaves at storage precision, counters."""
 
@@ -204,6 +258,28 @@ class Engine:
                         _lib.C128 if self.precision == "double" else _lib.C64)
         return DenseTensor.__new__(DenseTensor)._init_raw(plan.out_indices, contract_into(plan, lhs.data, rhs.data))
 
+    def absorb(self, s: LinearSchedule, run: list[int], assignment: dict[str, int], values: dict) -> DenseTensor:
+        """One fused K4 launch sequence for a stem run (see ``absorb_runs``):
+        the running tensor absorbs the run's leaf gates; same result legs as the
+        per-step contractions."""
+        from .fusion import absorb_chain
+
+        t = self.fetch(s, s.steps[run[0]].lhs, assignment, values)
+        gates = [self.fetch(s, s.steps[p].rhs, assignment, values) for p in run]
+        if self.precision != "single" or not t.data.is_contiguous():
+            out = t
+            for g in gates:
+                out = self.contract(out, g)
+            return out
+        return absorb_chain(t, gates)
+
+    def absorb_runs_for(self, s: LinearSchedule, sliced: frozenset, positions=None) -> dict[int, list[int]]:
+        key = (id(s), sliced, None if positions is None else tuple(positions))
+        cache = self.__dict__.setdefault("_runs", {})
+        if key not in cache:
+            cache[key] = absorb_runs(s, sliced, positions) if _fuse_enabled() and self.precision == "single" else {}
+        return cache[key]
+
     def run_range(self, s: LinearSchedule, lo: int, hi: int, assignment: dict[str, int], values: dict,
                   stats: RunStats, aux_bytes: int = 0, cache: dict | None = None,
                   invariant: set | frozenset = frozenset()) -> None:
@@ -215,12 +291,38 @@ class Engine:
         skipped."""
         rate = self.rate
         live = sum(v.size for v in values.values())
+        runs = self.absorb_runs_for(s, frozenset(assignment)) if self.cap is None and not invariant else {}
+        skip_to = -1
         for pos in range(lo - 1, hi):
+            if pos < skip_to:
+                continue
             step = s.steps[pos]
             if step.result in invariant:
                 if step.result in cache:
                     values[step.result] = cache[step.result]
                     live += values[step.result].size
+                continue
+            run = runs.get(pos)
+            if run is not None and run[-1] < hi:
+                out = self.absorb(s, run, assignment, values)
+                cur = [ix for ix in s.indices_of(s.steps[run[0]].lhs) if ix.label not in assignment]
+                for p in run:
+                    g = [ix for ix in s.indices_of(s.steps[p].rhs) if ix.label not in assignment]
+                    stats.multiplies += multiply_cost(cur, g)
+                    cur_set = {ix.label for ix in g}
+                    nxt = [ix for ix in cur if ix.label not in cur_set] + \
+                          [ix for ix in g if ix.label not in {c.label for c in cur}]
+                    stats.bytes_moved += (product(ix.dim for ix in cur) + product(ix.dim for ix in g)
+                                          + product(ix.dim for ix in nxt)) * rate
+                    cur = nxt
+                first = s.steps[run[0]].lhs
+                if first >= s.n_leaves and first in values:
+                    live -= values[first].size
+                    del values[first]
+                values[s.steps[run[-1]].result] = out
+                live += out.size
+                stats.bytes_peak = max(stats.bytes_peak, live * rate + aux_bytes)
+                skip_to = run[-1] + 1
                 continue
             lhs = self.fetch(s, step.lhs, assignment, values)
             rhs = self.fetch(s, step.rhs, assignment, values)
@@ -594,8 +696,20 @@ class SliceExecutor:
         else:
             # lean loop: hundreds of tiny steps, so no per-step accounting
             # (SSA values are consumed exactly once; the totals are exact)
+            runs = eng.absorb_runs_for(s, frozenset(self.spec.labels), self.invariant_positions)
+            skip_to = -1
             for p in self.invariant_positions:
+                if p < skip_to:
+                    continue
                 st = s.steps[p]
+                run = runs.get(p)
+                if run is not None:  # stem chain -> one fused absorb
+                    out = eng.absorb(s, run, {}, values)
+                    if st.lhs >= s.n_leaves:
+                        values.pop(st.lhs, None)
+                    values[s.steps[run[-1]].result] = out
+                    skip_to = run[-1] + 1
+                    continue
                 out = eng.contract(eng.fetch(s, st.lhs, {}, values), eng.fetch(s, st.rhs, {}, values))
                 for ref in (st.lhs, st.rhs):
                     if ref >= s.n_leaves:
@@ -613,8 +727,21 @@ class SliceExecutor:
         values = dict(self.cache)
         eng = self.eng
         s = self.s
+        runs = eng.absorb_runs_for(s, frozenset(self.spec.labels), self.dependent_positions)
+        skip_to = -1
         for p in self.dependent_positions:
+            if p < skip_to:
+                continue
             step = s.steps[p]
+            run = runs.get(p)
+            if run is not None:  # stem chain -> one fused absorb
+                out = eng.absorb(s, run, assignment, values)
+                ref = step.lhs
+                if ref >= s.n_leaves and ref in values and ref not in self.cache:
+                    del values[ref]
+                values[s.steps[run[-1]].result] = out
+                skip_to = run[-1] + 1
+                continue
             lhs = eng.fetch(s, step.lhs, assignment, values)
             rhs = eng.fetch(s, step.rhs, assignment, values)
             out = eng.contract(lhs, rhs)

@@ -95,3 +95,59 @@ def test_c2_plan_is_two_passes(cuda_ready):
     axes, _, _ = plan_chain(t, gs)
     passes, groups = chain_info(30, axes)
     assert passes == 2, (passes, groups)
+
+
+def _chain_network(rank, n_gates, seed):
+    from paper_2504_09186_b200 import ContractionTree, DenseTensor, Index, TensorNetwork
+    from paper_2504_09186_b200.workloads import ChainCase
+
+    t_labels, data, gates = ChainCase(rank, n_gates, seed).build()
+    leaves = [DenseTensor([Index(l) for l in t_labels], data)]
+    leaves += [DenseTensor([Index(oa), Index(ob), Index(ia), Index(ib)], u) for ia, ib, oa, ob, u in gates]
+    net = TensorNetwork(leaves)
+    n = len(leaves)
+    path = [[0, 1]] + [[n + i, i + 2] for i in range(n_gates - 1)]  # absorb the gates in order
+    tree = ContractionTree.from_ssa_path([tuple(t.indices) for t in leaves], path)
+    return t_labels, data, gates, net, tree
+
+
+def test_executor_fuses_stem_chain(cuda_ready, monkeypatch):
+    """A contraction path that absorbs gate leaves one by one into a rank-18
+    tensor: the executor finds the stem run (reference tree.py:278-330) and
+    dispatches it to the fused K4 chain -- absorb launches replace the
+    per-gate steps, the result and the multiply count are unchanged."""
+    import ctypes
+
+    from paper_2504_09186_b200 import _lib, linearize, tree_metrics
+    from paper_2504_09186_b200.execute import absorb_runs, run_open
+
+    t_labels, data, gates, net, tree = _chain_network(18, 12, 11)
+    s = linearize(tree)
+    runs = absorb_runs(s)
+    assert len(runs) == 1 and len(next(iter(runs.values()))) == 12
+    ref = (tuple(t_labels), (2,) * 18, data.astype(np.complex128))
+    for ia, ib, oa, ob, u in gates:
+        ref = tncref.contract(ref, ((oa, ob, ia, ib), (2, 2, 2, 2), u.astype(np.complex128)))
+    lib = _lib.load()
+    lib.tnc_profile_enable(1)
+    got = run_open(net, tree)
+    n = ctypes.c_int64()
+    ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    lib.tnc_profile_read(5, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by))
+    lib.tnc_profile_enable(0)
+    assert n.value >= 1  # fused absorb pass(es) ran
+    assert list(got.labels) == list(ref[0])
+    assert rel_l2(got.numpy(), ref[2]) <= 1e-5
+    # the reference step loop (run_range) fuses too, with the reference counters
+    from paper_2504_09186_b200.execute import Engine, RunStats
+
+    eng = Engine(net, "single")
+    st = RunStats()
+    vals = {}
+    eng.run_range(s, 1, len(s.steps), {}, vals, st)
+    assert st.multiplies == tree_metrics(tree).total_cost
+    assert rel_l2(vals[s.steps[-1].result].numpy(), ref[2]) <= 1e-5
+    # and with fusion switched off the per-gate path gives the same tensor
+    monkeypatch.setenv("TNC_FUSE_ABSORB", "0")
+    plain = run_open(net, tree)
+    assert rel_l2(plain.numpy(), got.numpy()) <= 1e-5
