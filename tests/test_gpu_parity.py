@@ -395,6 +395,56 @@ def test_open_output_spindle_reuse(cuda_ready):
     assert rr.stats.multiplies <= rep3.predicted_multiplies
 
 
+def _sliced_fixture_plan(max_k):
+    from paper_2504_09186_b200 import (
+        choose_reuse_subset, circuit_to_network, greedy_path, parse_circuit, select_slices,
+    )
+
+    g = load_golden("sliced")
+    circ = parse_circuit(g["circuit"])
+    net = circuit_to_network(circ, "0" * circ.n_qubits)
+    t = greedy_path(net, 0)
+    spec = select_slices(t, 7, 64, 0)
+    return g, net, t, spec, choose_reuse_subset(t, spec, None, max_k)
+
+
+def test_tree_reuse_program_on_device(cuda_ready):
+    """Tree-reuse action programs (reference reuse.py:257-283 _emit_tree,
+    351-364 plan_tree_reuse) run by the device interpreter: same value as the
+    reference's sliced sum, and the multiply count the program implies."""
+    from paper_2504_09186_b200 import plan_spindle, run_reuse
+    from paper_2504_09186_b200.reuse import plan_tree_reuse
+
+    g, net, t, spec, part = _sliced_fixture_plan(12)
+    rt = plan_tree_reuse(part.schedule, part.spec, nested_labels=part.nested_labels)
+    assert {a.kind for a in rt.actions} <= {"RUN", "CHECKPOINT", "RESTORE", "FREE"}
+    res = run_reuse(net, t, rt, 1, "single")
+    want = complex(*g["value"])
+    assert abs(res.value - want) <= TOL_C64 * abs(want)
+    _, rep = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    assert rep.predicted_multiplies <= res.stats.multiplies  # the spindle merges; the tree only forks
+
+
+def test_tune_memory_budget_on_device(cuda_ready):
+    """tune_memory (reference reuse.py:396-439) displaces forks / merges until
+    the spindle peak fits a device byte budget; the tuned program runs under
+    that budget on the device, stays within it and gives the reference value."""
+    from paper_2504_09186_b200 import plan_spindle, run_reuse
+    from paper_2504_09186_b200.reuse import tune_memory
+
+    g, net, t, spec, part = _sliced_fixture_plan(3)
+    _, rep = plan_spindle(part.schedule, part.spec, None, nested_labels=part.nested_labels)
+    budget = int(0.8 * rep.predicted_peak_bytes)
+    tr = tune_memory(part.schedule, part.spec, budget, nested_labels=part.nested_labels)
+    rs2, rep2 = plan_spindle(part.schedule, tr.spec, None, nested_labels=tr.nested_labels)
+    assert rep2.predicted_peak_bytes <= budget < rep.predicted_peak_bytes
+    res = run_reuse(net, t, rs2, 1, "single", mem_budget=budget)
+    want = complex(*g["value"])
+    assert abs(res.value - want) <= TOL_C64 * abs(want)
+    assert res.stats.multiplies == rep2.predicted_multiplies
+    assert res.stats.bytes_peak <= budget
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_fused_gather_split_bitwise(cuda_ready, seed, monkeypatch):
     """The K1 gather fused with the 3xFP16 split writes the same planes as
