@@ -62,7 +62,7 @@ def main():
         "device_peak_gib_during_prefix": peak / 2 ** 30,
         "device_resident_before_prefix_gib (leaves + slice-invariant cache)": base_mem / 2 ** 30,
         "predicted_multiplies_all": str(rep.predicted_multiplies),
-        "overhead_with_reuse": rep.overhead_with_reuse if hasattr(rep, "overhead_with_reuse") else None,
+        "overhead_with_reuse": float(rep.overhead_with_reuse) if hasattr(rep, "overhead_with_reuse") else None,
         "plan_s": t_plan, "prepare_s": t_prep, "prefix_s": t_run, "prefix_end": err,
         "device": torch.cuda.get_device_name(0),
     }, indent=1))
