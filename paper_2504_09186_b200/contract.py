@@ -76,7 +76,7 @@ class ContractPlan:
         return int(self.info.workspace_bytes)
 
     def __del__(self):
-        lib = _lib._lib
+        lib = _lib._lib if _lib is not None else None  # module globals are gone at interpreter exit
         if lib is not None and self.handle:
             lib.tnc_plan_destroy(self.handle)
             self.handle = 0

@@ -38,6 +38,7 @@
 // k-block g-1 right after staging k-block g (one elected lane).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -68,6 +69,7 @@ struct GtParams {
   const int64_t* tabs;  // [kGtTabs][4][256] outer-index offset tables
   int64_t m_blocks, kblocks, mn;
   int splits, chunk_kb;
+  int spin;             // stage / TMEM barrier waits poll without a suspend hint
   int rbits, fy;        // real row / column bits (phantom bits, stride 0, sit above)
   // tile bit j (thread bit j for j < 8, iteration bit j - 8 above): element
   // offset in the operand and XOR-linear smem byte address in the stage plane
@@ -82,8 +84,9 @@ struct GtParams {
   int64_t dxm[32], dom[32], dcm[32];
 };
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
+template <int NMMA, int KBC, int STAGES, bool PX, int YM>
 struct GtCfg {
+  static constexpr bool PY = YM == 1;  // Y pairs are 16 contiguous bytes in HBM
   static constexpr int kLogK = KBC == 32 ? 5 : 4;
   static constexpr int kLogN = NMMA == 32 ? 4 : NMMA == 64 ? 5 : NMMA == 128 ? 6 : 7;  // log2(NMMA / 2)
   // tile bits of the gathered element grid (a paired leg is inside the element)
@@ -105,6 +108,7 @@ struct GtCfg {
   static constexpr uint32_t kIdesc = idesc_f32acc(2, 128, NMMA);
   static_assert(kSmem + 4096 <= 227 * 1024, "smem budget");
   static_assert(kXBits >= 8 && kYBits >= 8, "tile smaller than the CTA");
+  static_assert((PX || kXPer >= 2) && (YM != 0 || kYPer >= 2), "register pairs need two elements per thread");
 };
 
 __device__ __forceinline__ int64_t tab4(const int64_t* t, int64_t idx) {
@@ -211,9 +215,9 @@ struct GtCursor {
   }
 };
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
+template <int NMMA, int KBC, int STAGES, bool PX, int YM>
 __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
-  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, YM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
@@ -312,6 +316,11 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
   float acc[Cfg::kHalf];
 #pragma unroll
   for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
+  const bool spin = p.spin != 0;
+  auto wait = [&](uint64_t* bar, uint32_t parity) {
+    if (spin) mbar_wait_spin(bar, parity);
+    else mbar_wait(bar, parity);
+  };
 
   GtCursor pc;  // loads (one k-block ahead of the smem stores)
   pc.init(p, units);
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     }
 #pragma unroll
     for (int i = 0; i < Cfg::kYPer; ++i) {
-      if constexpr (PY) vy[i] = __ldg(reinterpret_cast<const float4*>(yb + yoff(i)));
+      if constexpr (Cfg::PY) vy[i] = __ldg(reinterpret_cast<const float4*>(yb + yoff(i)));
       else vy[i] = __ldg(yb + yoff(i));
     }
     const int b = __ffs(pc.kb + 1) - 1;  // carry bit of kb -> kb + 1
@@ -388,12 +397,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       while (i_g < s0) {
         if (i_in_chunk == 0) {
           const uint32_t b = i_ch & 1;
-          mbar_wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
+          wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
           fence_after_sync();
           dcol = tmem_base + b * NMMA;
         }
         const uint32_t s = i_g % STAGES;
-        mbar_wait(&full[s], (i_g / STAGES) & 1);
+        wait(&full[s], (i_g / STAGES) & 1);
         fence_after_sync();
         const uint32_t st = smem0 + s * Cfg::kStage;
 #pragma unroll
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
     }
     if (have) {
       const uint32_t s = s0 % STAGES;
-      mbar_wait(&empty[s], ((s0 / STAGES) & 1) ^ 1);
+      wait(&empty[s], ((s0 / STAGES) & 1) ^ 1);
       const uint32_t st = smem0 + s * Cfg::kStage;
 #pragma unroll
       for (int i = 0; i < Cfg::kXPer; ++i) {
@@ -435,30 +444,41 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
           const float r0 = tf32_hi(cx[i].x), i0 = tf32_hi(cx[i].y), r1 = tf32_hi(cx[i].z), i1 = tf32_hi(cx[i].w);
           sts4(a, r0, i0, r1, i1);
           sts4(a + Cfg::kXPlane, cx[i].x - r0, cx[i].y - i0, cx[i].z - r1, cx[i].w - i1);
-        } else {
-          const float hr = tf32_hi(cx[i].x), hi = tf32_hi(cx[i].y);
-          sts2(a, hr, hi);
-          sts2(a + Cfg::kXPlane, cx[i].x - hr, cx[i].y - hi);
+        } else if ((i & 1) == 0) {
+          // register pair: elements i, i + 1 differ in k bit 0 (tile bit 8),
+          // 16 contiguous bytes of the plane
+          const float r0 = tf32_hi(cx[i].x), i0 = tf32_hi(cx[i].y);
+          const float r1 = tf32_hi(cx[i + 1].x), i1 = tf32_hi(cx[i + 1].y);
+          sts4(a, r0, i0, r1, i1);
+          sts4(a + Cfg::kXPlane, cx[i].x - r0, cx[i].y - i0, cx[i + 1].x - r1, cx[i + 1].y - i1);
         }
       }
 #pragma unroll
       for (int i = 0; i < Cfg::kYPer; ++i) {
         const uint32_t a0 = st + 2 * Cfg::kXPlane + yadr(i);
         const uint32_t a1 = a0 ^ 0x90u;  // row 2n+1 (row bit 0 and its swizzle bit)
-        if constexpr (PY) {
+        if constexpr (Cfg::PY) {
           const float r0 = tf32_hi(cy[i].x), i0 = tf32_hi(cy[i].y), r1 = tf32_hi(cy[i].z), i1 = tf32_hi(cy[i].w);
           const float lr0 = cy[i].x - r0, li0 = cy[i].y - i0, lr1 = cy[i].z - r1, li1 = cy[i].w - i1;
           sts4(a0, r0, -i0, r1, -i1);
           sts4(a1, i0, r0, i1, r1);
           sts4(a0 + Cfg::kYPlane, lr0, -li0, lr1, -li1);
           sts4(a1 + Cfg::kYPlane, li0, lr0, li1, lr1);
-        } else {
+        } else if constexpr (YM == 2) {
           const float hr = tf32_hi(cy[i].x), hi = tf32_hi(cy[i].y);
           const float lr = cy[i].x - hr, li = cy[i].y - hi;
           sts2(a0, hr, -hi);
           sts2(a1, hi, hr);
           sts2(a0 + Cfg::kYPlane, lr, -li);
           sts2(a1 + Cfg::kYPlane, li, lr);
+        } else if ((i & 1) == 0) {
+          const float r0 = tf32_hi(cy[i].x), i0 = tf32_hi(cy[i].y);
+          const float r1 = tf32_hi(cy[i + 1].x), i1 = tf32_hi(cy[i + 1].y);
+          const float lr0 = cy[i].x - r0, li0 = cy[i].y - i0, lr1 = cy[i + 1].x - r1, li1 = cy[i + 1].y - i1;
+          sts4(a0, r0, -i0, r1, -i1);
+          sts4(a1, i0, r0, i1, r1);
+          sts4(a0 + Cfg::kYPlane, lr0, -li0, lr1, -li1);
+          sts4(a1 + Cfg::kYPlane, li0, lr0, li1, lr1);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -476,7 +496,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
       const int64_t last = static_cast<int64_t>(f_base) + (end < f_n ? end : f_n) - 1;
       if (!drain && last + 2 > static_cast<int64_t>(s0)) break;
       const uint32_t b = ch & 1;
-      mbar_wait(&tfull[b], (ch >> 1) & 1);
+      wait(&tfull[b], (ch >> 1) & 1);
       fence_after_sync();
       const uint32_t taddr =
           tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + b * NMMA + half * Cfg::kHalf;
@@ -546,7 +566,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_c
 struct GatherTcPlan {
   GtParams p;
   GtParams p2;              // paired layout (16-byte K pairs), when pair_x
-  bool pair_x = false, pair_y = false;
+  bool pair_x = false;
+  int ymode = 0, ymode2 = 0;  // Y store mode of p / p2 (0 register pair, 1 memory pair, 2 unpaired)
   int nmma = 0, kbc = 0;
   int64_t rows_x = 0, rows_y = 0, k = 0;
   std::vector<int64_t> tabs_host;
@@ -707,29 +728,51 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   std::sort(yt.begin(), yt.end(), [&](int a, int b) { return legs[a].y_stride < legs[b].y_stride; });
 
   // ---- bit assignment: rows of R -> row bits, KL -> k bits, Y-free -> column
-  // bits.  A half-warp's 8-byte smem stores hit 16 distinct 8-byte slots iff
-  // the bank vectors of the operand's 4 fastest tile legs (thread bits 0-3)
-  // are independent; search the assignments that decide those vectors.
-  // Paired mode (px / py): the operand's stride-1 leg is a common leg placed on
-  // k bit 0, so each thread moves K-adjacent element pairs as 16 bytes (one
-  // global load, one store per plane); then a quarter-warp's 16-byte stores
-  // must hit 8 distinct 16-byte chunks (vectors over address bits 4-6 of the
-  // next 3 legs).
+  // bits.  Every smem store moves a K-adjacent element pair (16 bytes): one
+  // common tile leg L, the pair leg, sits on k bit 0.
+  //   memory pair (px / py): L is the operand's stride-1 leg, so the pair is
+  //     also 16 contiguous bytes in HBM (one 16-byte load); L is inside the
+  //     element, not a tile bit;
+  //   register pair (otherwise): L is tile bit 8, the thread's first
+  //     iteration bit, so its elements 2m and 2m + 1 are the pair (two 8-byte
+  //     loads, one 16-byte store per plane).
+  // A quarter-warp's 16-byte stores hit 8 distinct 16-byte chunks iff the
+  // chunk vectors (address bits 4-6) of the operand's 3 fastest tile legs
+  // (thread bits 0-2) are independent; search the assignments that decide them.
   const uint32_t xatom = 128 * 128, yatom = static_cast<uint32_t>(nmma) * 128;
-  auto assign = [&](bool px, bool py, GtParams& q) -> int {
+  // ymode: 0 register pair, 1 memory pair, 2 unpaired (8-byte Y stores; L keeps
+  // its place in Y's stride order, so Y's loads stay coalesced when L is one of
+  // Y's fast legs and Y is large)
+  auto assign = [&](bool px, int ymode, GtParams& q) -> int {
+    const bool py = ymode == 1;
     std::vector<int> row_of(n_legs, -1), k_of(n_legs, -1), n_of(n_legs, -1);
-    std::vector<int> xl(xt.begin() + (px ? 1 : 0), xt.end()), yl(yt.begin() + (py ? 1 : 0), yt.end());
-    const int xlanes = px ? 3 : 4, ylanes = py ? 3 : 4;
+    int L = xt[0];  // px: X's stride-1 leg
+    if (!px) {      // the common tile leg with the largest X stride (an iteration bit already, as a rule)
+      L = KL[0];
+      for (int leg : KL)
+        if (legs[leg].x_stride > legs[L].x_stride) L = leg;
+    }
+    std::vector<int> xl, yl;
+    for (int leg : xt)
+      if (leg != L) xl.push_back(leg);
+    for (int leg : yt)
+      if (leg != L || ymode == 2) yl.push_back(leg);
+    // a small Y stays in L1/L2 whatever its read order: its common legs take
+    // the thread bits, whose bank vectors the k-bit search below can always
+    // make independent
+    if (rows_y * 8 <= rows_x)
+      std::stable_partition(yl.begin(), yl.end(), [&](int leg) { return legs[leg].kind == 1; });
+    const int xlanes = 3, ylanes = ymode == 2 ? 4 : 3;
     const int nxl = std::min<int>(xlanes, static_cast<int>(xl.size()));
     const int nyl = std::min<int>(ylanes, static_cast<int>(yl.size()));
-    auto vec_row = [&](int j, bool chunk) { return chunk ? (j < 3 ? 1u << j : 0u) : (j < 3 ? (1u << (1 + j)) : 0u); };
-    auto vec_k = [&](int j, bool chunk) {
-      if (chunk) return (j >= 1 && j <= 3) ? 1u << (j - 1) : 0u;
-      return j == 0 ? 1u : (j <= 3 ? (1u << j) : 0u);
-    };
-    auto vec_n = [&](int j, bool chunk) { return chunk ? (j < 2 ? 1u << (j + 1) : 0u) : (j < 2 ? (1u << (2 + j)) : 0u); };
-    // smem store instructions per k-block
-    const double sx = (px ? 1.0 : 2.0) * 128 * kbc, sy = (py ? 2.0 : 4.0) * (nmma / 2) * kbc;
+    auto vec_row = [&](int j) { return j < 3 ? 1u << j : 0u; };
+    auto vec_k = [&](int j) { return (j >= 1 && j <= 3) ? 1u << (j - 1) : 0u; };
+    auto vec_n = [&](int j) { return j < 2 ? 1u << (j + 1) : 0u; };
+    // unpaired Y: a half-warp's 8-byte stores, 8-byte slots (address bits 3-6)
+    auto vec_k8 = [&](int j) { return j == 0 ? 1u : (j <= 3 ? (1u << j) : 0u); };
+    auto vec_n8 = [&](int j) { return j < 2 ? (1u << (2 + j)) : 0u; };
+    // smem store bytes per k-block
+    const double sx = 16.0 * 128 * kbc, sy = 32.0 * (nmma / 2) * kbc;
     std::vector<int> lowR, lowN;  // low-order legs whose slots matter
     for (int i = 0; i < nxl; ++i)
       if (legs[xl[i]].kind == 0) lowR.push_back(xl[i]);
@@ -762,7 +805,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
     enum_slots(static_cast<int>(lowN.size()), std::min(fy, 2), n_opts);
     do {
       for (size_t i = 0; i < KL.size(); ++i) k_of[KL[kperm[i]]] = static_cast<int>(i);
-      if (px && k_of[xt[0]] != 0) continue;  // the paired leg must sit on k bit 0
+      if (k_of[L] != 0) continue;  // the pair leg sits on k bit 0
       double bx = 1e300, by = 1e300;
       std::vector<int> br, bn;
       for (auto& ro : r_opts) {
@@ -770,10 +813,10 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
         for (int i = 0; i < nxl; ++i) {
           const int leg = xl[i];
           if (legs[leg].kind == 1) {
-            v[i] = vec_k(k_of[leg], px);
+            v[i] = vec_k(k_of[leg]);
           } else {
             const int sl = ro[std::find(lowR.begin(), lowR.end(), leg) - lowR.begin()];
-            v[i] = sl < 0 ? 0u : vec_row(sl, px);
+            v[i] = sl < 0 ? 0u : vec_row(sl);
           }
         }
         const double sc = sx * conflict_ways(v, nxl);
@@ -787,10 +830,10 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
         for (int i = 0; i < nyl; ++i) {
           const int leg = yl[i];
           if (legs[leg].kind == 1) {
-            v[i] = vec_k(k_of[leg], py);
+            v[i] = ymode == 2 ? vec_k8(k_of[leg]) : vec_k(k_of[leg]);
           } else {
             const int sl = no[std::find(lowN.begin(), lowN.end(), leg) - lowN.begin()];
-            v[i] = sl < 0 ? 0u : vec_n(sl, py);
+            v[i] = sl < 0 ? 0u : (ymode == 2 ? vec_n8(sl) : vec_n(sl));
           }
         }
         const double sc = sy * conflict_ways(v, nyl);
@@ -808,6 +851,9 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
       }
     } while (std::next_permutation(kperm.begin(), kperm.end()));
     for (size_t i = 0; i < KL.size(); ++i) k_of[KL[best_k[i]]] = static_cast<int>(i);
+    if (std::getenv("TNC_GT_DEBUG"))
+      std::fprintf(stderr, "tc_gather assign: nmma=%d kbc=%d px=%d ymode=%d store cost %.0f (conflict-free %.0f)\n", nmma,
+                   kbc, px, ymode, best_score, sx + sy);
     {  // rows: searched low legs first, the rest by output stride (lane-adjacent writes)
       std::vector<char> used(7, 0);
       for (size_t i = 0; i < lowR.size(); ++i)
@@ -841,27 +887,38 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
           used[slot] = 1;
         }
     }
-    // tile bit tables (a paired leg is the 16-byte element, not a bit)
-    uint64_t xsum = 0, ysum = 0;
-    int j = 0;
+    // tile bit tables: real legs by stride, phantom bits above them; a
+    // register pair leg goes to tile bit 8 (a memory pair leg is the 16-byte
+    // element, not a bit)
+    struct Bit {
+      uint32_t g, s;
+    };
+    std::vector<Bit> xb, yb;
+    uint64_t xsum = px ? 0 : static_cast<uint64_t>(legs[L].x_stride);
+    uint64_t ysum = ymode == 0 ? static_cast<uint64_t>(legs[L].y_stride) : 0;
     for (int leg : xl) {
       xsum += static_cast<uint64_t>(legs[leg].x_stride);
-      q.xg[j] = static_cast<uint32_t>(legs[leg].x_stride);
-      q.xs[j++] = legs[leg].kind == 0 ? row_bit_addr(row_of[leg]) : k_bit_addr(k_of[leg], xatom);
+      xb.push_back({static_cast<uint32_t>(legs[leg].x_stride),
+                    legs[leg].kind == 0 ? row_bit_addr(row_of[leg]) : k_bit_addr(k_of[leg], xatom)});
     }
-    for (int r = rb; r < 7; ++r) {  // phantom rows: re-read rows, never stored
-      q.xg[j] = 0;
-      q.xs[j++] = row_bit_addr(r);
-    }
-    j = 0;
+    for (int r = rb; r < 7; ++r) xb.push_back({0u, row_bit_addr(r)});  // phantom rows: re-read rows, never stored
+    if (!px) xb.insert(xb.begin() + 8, {static_cast<uint32_t>(legs[L].x_stride), k_bit_addr(0, xatom)});
     for (int leg : yl) {
       ysum += static_cast<uint64_t>(legs[leg].y_stride);
-      q.yg[j] = static_cast<uint32_t>(legs[leg].y_stride);
-      q.ys[j++] = legs[leg].kind == 2 ? row_bit_addr(n_of[leg] + 1) : k_bit_addr(k_of[leg], yatom);
+      yb.push_back({static_cast<uint32_t>(legs[leg].y_stride),
+                    legs[leg].kind == 2 ? row_bit_addr(n_of[leg] + 1) : k_bit_addr(k_of[leg], yatom)});
     }
-    for (int n = fy; n < lgn; ++n) {  // phantom columns
-      q.yg[j] = 0;
-      q.ys[j++] = row_bit_addr(n + 1);
+    for (int n = fy; n < lgn; ++n) yb.push_back({0u, row_bit_addr(n + 1)});  // phantom columns
+    if (ymode == 0) yb.insert(yb.begin() + 8, {static_cast<uint32_t>(legs[L].y_stride), k_bit_addr(0, yatom)});
+    if (xb.size() > static_cast<size_t>(kGtMaxBits) || yb.size() > static_cast<size_t>(kGtMaxBits))
+      TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: too many tile bits");
+    for (size_t j = 0; j < xb.size(); ++j) {
+      q.xg[j] = xb[j].g;
+      q.xs[j] = xb[j].s;
+    }
+    for (size_t j = 0; j < yb.size(); ++j) {
+      q.yg[j] = yb[j].g;
+      q.ys[j] = yb[j].s;
     }
     if (xsum + 1 >= (uint64_t{1} << 32) || ysum + 1 >= (uint64_t{1} << 32))
       TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: tile offsets exceed 32 bits");
@@ -886,7 +943,21 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   plan->k = int64_t{1} << c;
   p.rbits = rb;
   p.fy = fy;
-  if (const int st = assign(false, false, p); st != TNC_OK) {
+  // Y store mode without a memory pair: register pairs move the pair leg to
+  // Y's tile bit 8, which costs Y load coalescing when that leg is one of Y's
+  // 8 fastest tile legs -- only worth it while Y is small next to X
+  auto y_reg_pair_ok = [&](int L) {
+    const int pos = static_cast<int>(std::find(yt.begin(), yt.end(), L) - yt.begin());
+    return pos >= 8 || rows_y * 8 <= rows_x;
+  };
+  {
+    int L = KL[0];
+    for (int leg : KL)
+      if (legs[leg].x_stride > legs[L].x_stride) L = leg;
+    plan->ymode = y_reg_pair_ok(L) ? 0 : 2;
+    if (const char* env = std::getenv("TNC_GT_YMODE")) plan->ymode = std::atoi(env) == 2 ? 2 : 0;
+  }
+  if (const int st = assign(false, plan->ymode, p); st != TNC_OK) {
     delete plan;
     return st;
   }
@@ -955,10 +1026,9 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   const char* pair_env = std::getenv("TNC_GT_PAIR");
   if (px && !(pair_env && std::atoi(pair_env) == 0)) {
     plan->p2 = p;
-    if (assign(true, py, plan->p2) == TNC_OK) {
-      plan->pair_x = true;
-      plan->pair_y = py;
-    }
+    plan->ymode2 = py ? 1 : (y_reg_pair_ok(xt[0]) ? 0 : 2);
+    if (const char* env = std::getenv("TNC_GT_YMODE")) plan->ymode2 = std::atoi(env) == 2 ? 2 : (py ? 1 : 0);
+    if (assign(true, plan->ymode2, plan->p2) == TNC_OK) plan->pair_x = true;
   }
   const int up = upload_table(plan->tabs_host.data(), plan->tabs_host.size(), &plan->tabs_dev);
   if (up != TNC_OK) {
@@ -975,10 +1045,10 @@ void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
 
 namespace {
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
+template <int NMMA, int KBC, int STAGES, bool PX, int YM>
 int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
-  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
-  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY>;
+  using Cfg = GtCfg<NMMA, KBC, STAGES, PX, YM>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, YM>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
   ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
@@ -994,8 +1064,9 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
   if (!plan->tabs_dev && !plan->tabs_host.empty()) TNC_RET(TNC_ERR_INVALID, "tc_gather: plan tables missing");
   // paired layout when the plan has one and the operands are 16-byte aligned
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-                       (!plan->pair_y || (reinterpret_cast<uintptr_t>(y) & 15) == 0);
-  const bool px = plan->pair_x && aligned, py = px && plan->pair_y;
+                       (plan->ymode2 != 1 || (reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  const bool px = plan->pair_x && aligned;
+  const int ym = px ? plan->ymode2 : plan->ymode;
   GtParams p = px ? plan->p2 : plan->p;
   p.X = static_cast<const float2*>(x);
   p.Y = static_cast<const float2*>(y);
@@ -1008,21 +1079,28 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
   const double M = static_cast<double>(plan->rows_x), N = static_cast<double>(plan->rows_y),
                K = static_cast<double>(plan->k);
   const double flops = 8.0 * M * N * K, bytes = 8.0 * (M * K + N * K + M * N);
-#define TNC_GT_CASE(N, KBC, ST)                                                        \
-  case N:                                                                              \
-    if (py) return launch_gt<N, KBC, ST, true, true>(p, units, flops, bytes, stream);  \
-    if (px) return launch_gt<N, KBC, ST, true, false>(p, units, flops, bytes, stream); \
-    return launch_gt<N, KBC, ST, false, false>(p, units, flops, bytes, stream);
+  const char* spin_s = std::getenv("TNC_GT_SPIN");
+  p.spin = spin_s ? std::atoi(spin_s) : 1;
+#define TNC_GT_MODES(N, KBC, ST)                                                             \
+  do {                                                                                       \
+    if (px && ym == 1) return launch_gt<N, KBC, ST, true, 1>(p, units, flops, bytes, stream); \
+    if (px && ym == 0) return launch_gt<N, KBC, ST, true, 0>(p, units, flops, bytes, stream); \
+    if (px) return launch_gt<N, KBC, ST, true, 2>(p, units, flops, bytes, stream);            \
+    if (ym == 0) return launch_gt<N, KBC, ST, false, 0>(p, units, flops, bytes, stream);      \
+    return launch_gt<N, KBC, ST, false, 2>(p, units, flops, bytes, stream);                   \
+  } while (0)
   switch (plan->nmma) {
-    TNC_GT_CASE(32, 32, 2)
-    TNC_GT_CASE(64, 32, 2)
-    TNC_GT_CASE(128, 16, 3)
+    case 32: TNC_GT_MODES(32, 32, 2);
+    case 64: TNC_GT_MODES(64, 32, 2);
+    case 128: TNC_GT_MODES(128, 16, 3);
     case 256:
-      if (px) return launch_gt<256, 16, 2, true, false>(p, units, flops, bytes, stream);
-      return launch_gt<256, 16, 2, false, false>(p, units, flops, bytes, stream);
+      if (px && ym == 0) return launch_gt<256, 16, 2, true, 0>(p, units, flops, bytes, stream);
+      if (px) return launch_gt<256, 16, 2, true, 2>(p, units, flops, bytes, stream);
+      if (ym == 0) return launch_gt<256, 16, 2, false, 0>(p, units, flops, bytes, stream);
+      return launch_gt<256, 16, 2, false, 2>(p, units, flops, bytes, stream);
     default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
   }
-#undef TNC_GT_CASE
+#undef TNC_GT_MODES
 }
 
 }  // namespace tnc
