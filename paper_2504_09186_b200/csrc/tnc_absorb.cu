@@ -21,19 +21,26 @@
 //    and the next pass's tile axes come next (its reads are contiguous runs).
 //    C2 (16 random gates on a rank-30 tensor): 2 passes (3 with in-order
 //    sections of 12-bit tiles).
-//  * Pipeline.  One persistent CTA per SM, warp-specialised over a ring of 3
-//    tile buffers: 4 memory warps gather tile k (cp.async, mbarrier-tracked)
-//    and store tile k-1 while 8 math warps apply the pass's gates to the tile
-//    in between.  A pure copy pass runs at 6.4 TB/s (99 % of the measured HBM
-//    peak), so the pass time is max(HBM, gate math).
+//  * Pipeline.  One persistent CTA per SM (640 threads), warp-specialised over
+//    a ring of 3 tile buffers: 4 memory warps gather tile k (cp.async,
+//    mbarrier-tracked) and store tile k-2, and TWO math teams of 8 warps
+//    each own every other tile, so one team's shared-memory regrouping
+//    (cube loads / stores, team barrier) overlaps the other team's FP32 math.
+//    A pure copy pass runs at 6.4 TB/s (99 % of the measured HBM peak), so
+//    the pass time is max(HBM, gate math, tile regrouping).
 //  * Math.  Gates are grouped on <= 5 tile axes; each math thread holds a
 //    32-element register cube of the group's axes (256 threads x 32 = the
 //    tile) and applies the group's 4x4 gates with packed FP32 FMAs (FFMA2:
-//    2 per complex MAC).  The gate tables (oriented (re, re, -im, im) rows)
-//    are built on the device from the caller's device gate tensors: no host
-//    round trip.  (A tensor-core variant -- 16x16 group unitaries on
-//    mma.sync with a 3xFP16 split -- was correct but issue-bound at ~2 ms
-//    per group: commit d9b05fc.)
+//    2 per complex MAC).  The pass's gate coefficients sit in the constant
+//    bank (copied device-to-device from the table the table kernel builds
+//    from the caller's device gate tensors: no host round trip), so the
+//    FFMA2s take them as uniform-register operands and a math thread needs
+//    96 registers.  FFMA2 issues at 0.46 / clk / SM sub-partition
+//    (tools/ffma2_rate.cu): the same 118 FMA lanes / clk / SM as scalar
+//    FFMA in half the issue slots, which sets the FP32 floor of a pass.
+//    (A tensor-core variant -- 16x16 group unitaries on mma.sync with a
+//    3xFP16 split -- was correct but issue-bound at ~2 ms per group: commit
+//    d9b05fc.)
 //  * Banks.  8-byte smem slots are XOR-swizzled (swz); a tile bit's bank class
 //    is (bit mod 4).  The host places tile axes so that the 4 fastest load
 //    axes and the 4 fastest store axes each cover the 4 classes, and picks a
@@ -43,6 +50,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "tnc_common.cuh"
@@ -56,17 +64,22 @@ using namespace tc5;
 
 constexpr int kTB = 13;                       // tile bits
 constexpr int kTile = 1 << kTB;               // 8192 complex64 = 64 KB
-constexpr int kMathThreads = 256;             // 8 math warps: one 32-element cube per thread
+constexpr int kTeams = 2;                     // math teams, one tile each
+constexpr int kTeamThreads = 256;             // 8 math warps: one 32-element cube per thread
+constexpr int kMathThreads = kTeams * kTeamThreads;
 constexpr int kMemThreads = 128;              // 4 memory warps (HBM <-> smem)
 constexpr int kThreads = kMathThreads + kMemThreads;
-constexpr int kBufs = 3;                      // tile ring: loading / math / storing
+constexpr int kBufs = 3;                      // tile ring: loading or storing / team 0 / team 1
 constexpr int kMemPer = kTile / kMemThreads;  // 64 elements per memory thread per tile
 constexpr int kMemThrBits = 7;
 constexpr int kCubeBits = 5;
 constexpr int kCube = 1 << kCubeBits;
 constexpr int kMaxGroups = 24;                // groups per pass
-constexpr int kMaxPassGates = 64;             // gates per pass (tables in smem: 256 B each)
+constexpr int kMaxPassGates = 64;             // gates per pass (constant bank: 256 B each)
 constexpr int kMaxChainGates = 512;
+
+// The running pass's gate coefficients U[o][i] as (re, -im, im, 0), gate-major.
+__constant__ float4 c_gates[kMaxPassGates * 16];
 
 struct GroupParams {
   int cube_slot[kCubeBits];  // slot vectors of the cube (register-index) bits
@@ -80,6 +93,7 @@ struct AbsorbParams {
   int n_groups;
   int n_gates;               // gates of this pass
   int table_base;            // the pass's first gate in the device table
+  int teams;                 // math teams in use (2; 1 = A/B switch TNC_ABSORB_TEAMS)
   int64_t n_tiles;
   // memory-thread enumeration e = mt + 128 i: offset = thread part + [i] part
   int64_t in_bit[kMemThrBits];
@@ -96,7 +110,7 @@ struct AbsorbParams {
   int64_t outer_out[TNC_MAX_RANK];
 };
 
-// Device gate tables: entry j = 16 float4 (U[o][i] as (re, re, -im, im)) of
+// Device gate tables: entry j = 16 float4 (U[o][i] as (re, -im, im, 0)) of
 // chain gate src[j], oriented so that its in_a axis is the lower cube bit.
 struct TableParams {
   int n;
@@ -105,6 +119,9 @@ struct TableParams {
   const float2* gate[kMaxChainGates];
   int64_t gstride[kMaxChainGates][4];  // element strides of the (out_a, out_b, in_a, in_b) legs
 };
+
+// lowest set bit of n in [1, 31] (compile-time under full unrolling)
+__host__ __device__ constexpr int ctz5(int n) { return (n & 1) ? 0 : (n & 2) ? 1 : (n & 4) ? 2 : (n & 8) ? 3 : 4; }
 
 __host__ __device__ __forceinline__ int swz(int e) { return e ^ (((e >> 4) ^ (e >> 8) ^ (e >> 12)) & 15); }
 
@@ -139,20 +156,13 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
   return r;
 }
 
-// acc += u * x as two FFMA2 with no broadcast moves: the table holds
-// (u.re, u.re, -u.im, u.im) and xs = (x.im, x.re) is swapped once per element
+// 4x4 gate on cube bits (LA = in_a < LB = in_b) of a 32-element register
+// cube.  acc += u * x is two FFMA2 whose coefficient operands come from
+// uniform registers (the constant bank, warp-uniform gate index) and whose
+// half swaps are operand modifiers -- no moves, no negations:
 //   acc += (u.re, u.re) * (x.re, x.im) + (-u.im, u.im) * (x.im, x.re)
-__device__ __forceinline__ u64 cmac(u64 acc, float4 u, u64 x, u64 xs) {
-  acc = ffma2(as_u64(make_float2(u.x, u.y)), x, acc);
-  return ffma2(as_u64(make_float2(u.z, u.w)), xs, acc);
-}
-
-// 4x4 gate on cube bits (LA = in_a < LB = in_b) of a 32-element register cube
 template <int LA, int LB>
 __device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* u) {
-  float4 uu[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) uu[i] = u[i];  // shared memory, broadcast
 #pragma unroll
   for (int s = 0; s < kCube; ++s) {
     if ((s >> LA) & 1) continue;
@@ -168,7 +178,11 @@ __device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* u)
     for (int o = 0; o < 4; ++o) {
       u64 acc = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc = cmac(acc, uu[o * 4 + i], x[i], xs[i]);
+      for (int i = 0; i < 4; ++i) {
+        const float4 c = u[o * 4 + i];
+        acc = ffma2(bcast(c.x), x[i], acc);
+        acc = ffma2(as_u64(make_float2(c.y, c.z)), xs[i], acc);
+      }
       v[idx[o]] = as_f2(acc);
     }
   }
@@ -201,7 +215,7 @@ __global__ void absorb_table_kernel(const TableParams p, float4* __restrict__ ta
   const int oo = q(o), ii = q(i);
   const int64_t* st = p.gstride[g];
   const float2 u = p.gate[g][(oo >> 1) * st[0] + (oo & 1) * st[1] + (ii >> 1) * st[2] + (ii & 1) * st[3]];
-  table[16 * j + e] = make_float4(u.x, u.x, -u.y, u.y);
+  table[16 * j + e] = make_float4(u.x, -u.y, u.y, 0.f);
 }
 
 // Sum over the outer (non-tile) axes of tile t: one warp, lanes split the axes.
@@ -215,25 +229,28 @@ __device__ __forceinline__ int64_t tile_base(int64_t t, const int64_t* __restric
 }
 
 // One pass over the tensor, one persistent CTA per SM, warp-specialised over a
-// ring of 3 tile buffers (192 KB of smem):
-//   memory warps (4):  cp.async gather of tile k (HBM -> smem, 8-byte elements,
-//                      completion tracked by mbarrier full[b]), then the store
-//                      of tile k-1 (smem -> HBM in the output layout) once the
-//                      math warps released it (computed[b]), then empty[b];
-//   math warps (8):    the pass's gate groups on 32-element register cubes.
-// Loads, math and stores of three consecutive tiles overlap.
+// ring of 3 tile buffers (192 KB of smem); tile k of the CTA lives in buffer
+// k % 3 and belongs to math team k % 2:
+//   memory warps (4):  step k = cp.async gather of tile k (HBM -> smem, 8-byte
+//                      elements, completion tracked by mbarrier full[b]), then
+//                      the store of tile k-2 (smem -> HBM in the output layout)
+//                      once its team released it (computed[b]), then empty[b];
+//   math teams (2 x 8 warps): the pass's gate groups on 32-element register
+//                      cubes, one team barrier per group.
+// While one team regroups its tile through shared memory the other team's
+// FFMA2s have the FP32 pipe, and the loads / stores of two more tiles overlap.
 __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* __restrict__ in,
                                                                    float2* __restrict__ out,
-                                                                   const float4* __restrict__ table,
                                                                    const AbsorbParams p) {
-  extern __shared__ __align__(16) float2 tiles[];  // kBufs x kTile, then the pass's gate tables
-  __shared__ __align__(8) uint64_t full[kBufs], computed[kBufs], empty[kBufs];
+  extern __shared__ __align__(16) float2 tiles[];  // kBufs x kTile
+  __shared__ __align__(8) uint64_t full[kBufs], computed[kBufs], empty[kBufs], stagger;
   __shared__ int64_t s_oin[TNC_MAX_RANK], s_oout[TNC_MAX_RANK];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int warp = tid >> 5;
-  float4* su = reinterpret_cast<float4*>(tiles + kBufs * kTile);
-  for (int i = tid; i < 16 * p.n_gates; i += kThreads) su[i] = __ldg(table + 16 * p.table_base + i);
+  // warp-uniform by construction, and visibly so to the compiler: the role
+  // branches are then convergent and the gate coefficients can ride the
+  // uniform datapath
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   if (tid < p.n_outer) {
     s_oin[tid] = p.outer_in[tid];
     s_oout[tid] = p.outer_out[tid];
@@ -244,11 +261,13 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
       mbar_init(&computed[b], 1);
       mbar_init(&empty[b], kMemThreads);
     }
+    mbar_init(&stagger, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (warp >= kMathThreads / 32) {
-    // ---- memory warps
+    // ---- memory warps (one warpgroup): hand registers to the math warpgroups
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
     const int mt = tid - kMathThreads;
     int64_t my_in = 0, my_out = 0;
     int my_in_slot = 0, my_out_slot = 0;
@@ -263,8 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
     const uint32_t tiles_s = smem_u32(tiles);
     for (int64_t k = 0;; ++k) {
       const int64_t t = blockIdx.x + k * gridDim.x;
-      const bool have = t < p.n_tiles;
-      if (have) {
+      if (t < p.n_tiles) {
         const int b = static_cast<int>(k % kBufs);
         if (k >= kBufs) mbar_wait(&empty[b], static_cast<uint32_t>((k / kBufs - 1) & 1));
         const float2* src = in + tile_base(t, s_oin, p.n_outer, lane) + my_in;
@@ -273,21 +291,31 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
         for (int i = 0; i < kMemPer; ++i) cp_async8(dst + ((my_in_slot ^ p.in_slot_i[i]) << 3), src + p.in_i[i]);
         cp_async_arrive(&full[b]);
       }
-      if (k >= 1) {
-        const int64_t kp = k - 1;
+      if (k >= p.teams) {
+        const int64_t kp = k - p.teams;
+        const int64_t tp = blockIdx.x + kp * gridDim.x;
+        if (tp >= p.n_tiles) break;
         const int bp = static_cast<int>(kp % kBufs);
         mbar_wait(&computed[bp], static_cast<uint32_t>((kp / kBufs) & 1));
         const float2* tile = tiles + bp * kTile;
-        float2* dst = out + tile_base(t - gridDim.x, s_oout, p.n_outer, lane) + my_out;
+        float2* dst = out + tile_base(tp, s_oout, p.n_outer, lane) + my_out;
 #pragma unroll 16
         for (int i = 0; i < kMemPer; ++i) __stcs(dst + p.out_i[i], tile[my_out_slot ^ p.out_slot_i[i]]);
         mbar_arrive(&empty[bp]);
       }
-      if (!have) break;
     }
   } else {
-    // ---- math warps
-    for (int64_t k = 0;; ++k) {
+    // ---- math teams (warpgroups 0-3): 640 x 96 registers at launch, 512 x 112 + 128 x 40 now
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    const int team = warp >> 3;
+    const int tw = warp & 7;
+    // Team 1 starts half a tile behind team 0 (released when team 0 is half
+    // way through the groups of its first tile) and the teams stay in
+    // anti-phase from there: nothing else would separate them, and two teams
+    // in phase regroup at the same time and do their math at the same time.
+    if (team >= p.teams) return;
+    if (team == 1) mbar_wait(&stagger, 0);
+    for (int64_t k = team;; k += p.teams) {
       const int64_t t = blockIdx.x + k * gridDim.x;
       if (t >= p.n_tiles) break;
       const int b = static_cast<int>(k % kBufs);
@@ -301,31 +329,33 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
           if ((lane >> j) & 1) base ^= gp.lane_slot[j];
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if ((warp >> j) & 1) base ^= gp.warp_slot[j];
+          if ((tw >> j) & 1) base ^= gp.warp_slot[j];
         int sb[kCubeBits];
 #pragma unroll
         for (int j = 0; j < kCubeBits; ++j) sb[j] = gp.cube_slot[j];
+        // cube elements in Gray-code order: one running address, one XOR with a
+        // uniform slot vector per element (no table of 32 addresses kept live)
         float2 c[kCube];
+        int a = base;
 #pragma unroll
-        for (int s = 0; s < kCube; ++s) {
-          int a = base;
-#pragma unroll
-          for (int j = 0; j < kCubeBits; ++j)
-            if ((s >> j) & 1) a ^= sb[j];
-          c[s] = tile[a];
+        for (int n = 0; n < kCube; ++n) {
+          if (n > 0) a ^= sb[ctz5(n)];
+          c[n ^ (n >> 1)] = tile[a];
         }
-        for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], su + 16 * k2);
+        for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], c_gates + 16 * k2);
+        asm volatile("mov.b32 %0, %1;" : "=r"(a) : "r"(base));  // recompute, do not keep, the addresses
 #pragma unroll
-        for (int s = 0; s < kCube; ++s) {
-          int a = base;
-#pragma unroll
-          for (int j = 0; j < kCubeBits; ++j)
-            if ((s >> j) & 1) a ^= sb[j];
-          tile[a] = c[s];
+        for (int n = 0; n < kCube; ++n) {
+          if (n > 0) a ^= sb[ctz5(n)];
+          tile[a] = c[n ^ (n >> 1)];
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kMathThreads) : "memory");
+        // team barrier (ids 1, 2): the next group's cubes cross the team's warps
+        if (team == 0) asm volatile("bar.sync 1, %0;" ::"n"(kTeamThreads) : "memory");
+        else asm volatile("bar.sync 2, %0;" ::"n"(kTeamThreads) : "memory");
+        if (k == 0 && tid == 0 && g == (p.n_groups - 1) / 2) mbar_arrive(&stagger);
       }
-      if (tid == 0) mbar_arrive(&computed[b]);
+      if (k == 0 && tid == 0 && p.n_groups == 0) mbar_arrive(&stagger);
+      if ((tid & (kTeamThreads - 1)) == 0) mbar_arrive(&computed[b]);
     }
   }
 }
@@ -584,6 +614,10 @@ int build_pass_params(int r, const Pass& ps, const std::vector<GateRef>& gates_o
   p.n_tiles = static_cast<int64_t>(1) << p.n_outer;
   p.n_groups = static_cast<int>(ps.groups.size());
   p.table_base = table_base;
+  {
+    const char* e = std::getenv("TNC_ABSORB_TEAMS");
+    p.teams = (e && std::atoi(e) == 1) ? 1 : kTeams;
+  }
   // each group: 5 cube bits (its axes + padding), 5 lane bits (the first 4
   // of distinct bank classes), 3 warp bits; gates oriented so in_a is the
   // lower cube bit
@@ -698,6 +732,16 @@ int plan_chain(int r, int n_gates, const int32_t* axes, ChainPlan& cp) {
 // gate tables: 16 float4 per gate
 size_t table_bytes(int n_gates) { return (static_cast<size_t>(std::max(n_gates, 1)) * 256 + 255) & ~size_t(255); }
 
+// c_gates is one per device: chains launched on different streams take turns
+// (the later stream waits for the earlier chain's last pass).
+struct ConstOwner {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  bool used = false;
+};
+std::mutex g_const_mu;
+ConstOwner g_const_owner[64];
+
 }  // namespace
 
 int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t* bytes) {
@@ -747,25 +791,37 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
     absorb_table_kernel<<<tp.n, 16, 0, stream>>>(tp, table);
     TNC_CHECK_LAUNCH();
   }
-  int max_gates = 0;
-  for (const auto& prm : params) max_gates = std::max(max_gates, prm.n_gates);
-  const size_t smem = static_cast<size_t>(kBufs) * kTile * sizeof(float2) + static_cast<size_t>(max_gates) * 256;
+  const size_t smem = static_cast<size_t>(kBufs) * kTile * sizeof(float2);
   TNC_CUDA_TRY(cudaFuncSetAttribute(absorb_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
+  int dev = 0;
+  TNC_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) TNC_RET(TNC_ERR_UNSUPPORTED, "absorb: device index out of range");
+  std::lock_guard<std::mutex> lock(g_const_mu);
+  ConstOwner& owner = g_const_owner[dev];
+  if (!owner.done) TNC_CUDA_TRY(cudaEventCreateWithFlags(&owner.done, cudaEventDisableTiming));
+  if (owner.used && owner.stream != stream) TNC_CUDA_TRY(cudaStreamWaitEvent(stream, owner.done, 0));
   const float2* cur = static_cast<const float2*>(t_in);
   for (int k = 0; k < P; ++k) {
     float2* dst = ((P - 1 - k) % 2 == 0) ? static_cast<float2*>(t_out) : ws;
     const AbsorbParams& p = params[k];
     const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()));
+    if (p.n_gates > 0)
+      TNC_CUDA_TRY(cudaMemcpyToSymbolAsync(c_gates, table + 16 * p.table_base,
+                                           static_cast<size_t>(p.n_gates) * 16 * sizeof(float4), 0,
+                                           cudaMemcpyDeviceToDevice, stream));
     {
       // algorithmic work: 16 complex MACs (64 real flops) per 4 elements per gate
       ProfScope prof(PROF_ABSORB, 32.0 * p.n_gates * static_cast<double>(int64_t(1) << r),
                      16.0 * static_cast<double>(int64_t(1) << r), stream);
-      absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(cur, dst, table, p);
+      absorb_pass_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(cur, dst, p);
       TNC_CHECK_LAUNCH();
     }
     cur = dst;
   }
+  TNC_CUDA_TRY(cudaEventRecord(owner.done, stream));
+  owner.stream = stream;
+  owner.used = true;
   return TNC_OK;
 }
 
