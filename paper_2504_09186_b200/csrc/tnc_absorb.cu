@@ -320,34 +320,36 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
       if (t >= p.n_tiles) break;
       const int b = static_cast<int>(k % kBufs);
       mbar_wait(&full[b], static_cast<uint32_t>((k / kBufs) & 1));
-      float2* tile = tiles + b * kTile;
+      char* tile_b = reinterpret_cast<char*>(tiles + b * kTile);
       for (int g = 0; g < p.n_groups; ++g) {
         const GroupParams& gp = p.g[g];
-        int base = 0;
+        // byte offsets inside the tile buffer: the running XOR is the whole
+        // per-element address arithmetic (the buffer base is uniform)
+        uint32_t base = 0;
 #pragma unroll
         for (int j = 0; j < 5; ++j)
-          if ((lane >> j) & 1) base ^= gp.lane_slot[j];
+          if ((lane >> j) & 1) base ^= static_cast<uint32_t>(gp.lane_slot[j]) << 3;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          if ((tw >> j) & 1) base ^= gp.warp_slot[j];
-        int sb[kCubeBits];
+          if ((tw >> j) & 1) base ^= static_cast<uint32_t>(gp.warp_slot[j]) << 3;
+        uint32_t sb[kCubeBits];
 #pragma unroll
-        for (int j = 0; j < kCubeBits; ++j) sb[j] = gp.cube_slot[j];
-        // cube elements in Gray-code order: one running address, one XOR with a
+        for (int j = 0; j < kCubeBits; ++j) sb[j] = static_cast<uint32_t>(gp.cube_slot[j]) << 3;
+        // cube elements in Gray-code order: one running offset, one XOR with a
         // uniform slot vector per element (no table of 32 addresses kept live)
         float2 c[kCube];
-        int a = base;
+        uint32_t a = base;
 #pragma unroll
         for (int n = 0; n < kCube; ++n) {
           if (n > 0) a ^= sb[ctz5(n)];
-          c[n ^ (n >> 1)] = tile[a];
+          c[n ^ (n >> 1)] = *reinterpret_cast<const float2*>(tile_b + a);
         }
         for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], c_gates + 16 * k2);
         asm volatile("mov.b32 %0, %1;" : "=r"(a) : "r"(base));  // recompute, do not keep, the addresses
 #pragma unroll
         for (int n = 0; n < kCube; ++n) {
           if (n > 0) a ^= sb[ctz5(n)];
-          tile[a] = c[n ^ (n >> 1)];
+          *reinterpret_cast<float2*>(tile_b + a) = c[n ^ (n >> 1)];
         }
         // team barrier (ids 1, 2): the next group's cubes cross the team's warps
         if (team == 0) asm volatile("bar.sync 1, %0;" ::"n"(kTeamThreads) : "memory");
