@@ -520,6 +520,23 @@ def bench_dry(args) -> None:
         dist.destroy_process_group()
 
 
+FMA_LANES_PER_CLK_PER_SM = 118.0  # measured: tools/ffma2_rate.cu -> profiles/r02_ffma2_rate.txt
+
+
+def _fp32_floor(n_gates: int, n_elems: int, seconds: float) -> dict:
+    """FP32-pipe time of a gate chain (16 real FMAs per element per gate) at the
+    measured FMA issue rate, at the maximum SM clock (the K4 passes run
+    unthrottled), and the fraction of it the fused chain reached."""
+    import torch
+
+    prop = torch.cuda.get_device_properties(0)
+    sm_hz = measured_peaks().get("sm_max_mhz", 1965.0) * 1e6
+    fmas = 16.0 * n_gates * n_elems
+    floor = fmas / (FMA_LANES_PER_CLK_PER_SM * prop.multi_processor_count * sm_hz)
+    return {"ms": floor * 1e3, "frac": floor / seconds, "fma_lanes_per_clk_per_sm": FMA_LANES_PER_CLK_PER_SM,
+            "sm_mhz": sm_hz / 1e6}
+
+
 def bench_c2(args) -> None:
     """Config C2: rank-30 tensor (8 GiB) absorbing 16 random two-qubit gates --
     fused K4 chain vs 16 separate contract_pair passes (HBM-bound)."""
@@ -574,6 +591,10 @@ def bench_c2(args) -> None:
         "roofline": {"bound": "hbm", "achieved": nbytes / fused_t / 1e9, "peak": peaks.get("hbm_gbs"),
                      "unit": "GB/s", "frac": nbytes / fused_t / 1e9 / peaks.get("hbm_gbs"), "traffic": None,
                      "kernel": "absorb_pass_kernel", "note": "algorithmic bytes = one read + one write of T"},
+        # The gate math runs on the FP32 pipe: 16 real FMAs per element per gate
+        # against the measured 118 FMA lanes / clk / SM (FFMA and FFMA2 alike,
+        # profiles/r02_ffma2_rate.txt) at the SM clock the kernel ran at.
+        "fp32_floor": _fp32_floor(len(gs), 1 << 30, fused_t),
         "kernels": prof,
     }
     print(json.dumps(line), flush=True)
