@@ -612,6 +612,7 @@ def bench_c1(args) -> None:
     torch.cuda.set_device(0)
     lib = _lib.load(require_device=True)
     peaks = measured_peaks()
+    tf32 = measure_tf32_peak(0.5)
     for case in c1_cases():
         ia, ib, io = case.index_lists()
         da, db = case.data()
@@ -644,10 +645,22 @@ def bench_c1(args) -> None:
         n = 2 ** sum(1 for l in case.b_labels if l.startswith("b"))
         flops = 8.0 * m * k * n
         nbytes = 8.0 * (m * k + k * n + m * n)
+        # step roofline: max(algorithmic bytes / HBM peak, flops / P_eff), burst peaks
+        # (the kernel is timed alone); P_eff = the split scheme's tensor rate / 3 products
+        f16 = prof["tc_gemm"]["launches"] > 0
+        p_eff = (peaks.get("bf16_tflops", 1590.0) if f16 else tf32["tf32_tflops"]) / 3.0
+        t_hbm, t_tc = nbytes / (peaks.get("hbm_gbs") * 1e9), flops / (p_eff * 1e12)
+        bound = "tensor" if t_tc > t_hbm else "hbm"
+        roof = ({"bound": "tensor", "achieved": flops / dt / 1e12, "peak": p_eff, "unit": "TFLOP/s"} if bound == "tensor"
+                else {"bound": "hbm", "achieved": nbytes / dt / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s"})
+        roof.update({"frac": max(t_hbm, t_tc) / dt, "traffic": None, "hbm_floor_ms": t_hbm * 1e3,
+                     "tensor_floor_ms": t_tc * 1e3,
+                     "scheme": "3xFP16 (bf16_tflops / 3)" if f16 else "3xTF32 (TF32 burst measured this run / 3)"})
         print(json.dumps({"metric": f"{case.name} contract+permute", "value": flops / dt / 1e12, "unit": "TFLOP/s",
                           "ms_per_step": dt * 1e3, "GB_per_s_algorithmic": nbytes / dt / 1e9,
-                          "hbm_frac": nbytes / dt / 1e9 / peaks.get("hbm_gbs"), "shape_log2": [
-                              m.bit_length() - 1, k.bit_length() - 1, n.bit_length() - 1], "kernels": prof}),
+                          "hbm_frac": nbytes / dt / 1e9 / peaks.get("hbm_gbs"), "roofline": roof, "shape_log2": [
+                              m.bit_length() - 1, k.bit_length() - 1, n.bit_length() - 1],
+                          "tf32_measured_this_run": tf32, "kernels": prof}),
               flush=True)
         del a, b, out, plan
 
