@@ -5,9 +5,10 @@ Semantics are exactly the reference's repeated ``contract_pair(T, G)``
 four legs, two of them shared with the current T; the result legs are
 free_T (T's order) ++ free_G (G's order).  The device path is
 ``tnc_absorb_chain``: the chain runs in the fewest shared-memory-tiled HBM
-passes the tile allows (2 for C2), with the gates multiplied into 3-axis
-group unitaries on the device and applied on tensor cores -- instead of one
-permute + GEMM round trip per gate.  Gate values never leave the device.
+passes the tile allows (2 for C2); within a pass the gates are applied to
+32-element register cubes with packed FP32 FMAs whose coefficients come from
+the constant bank -- instead of one permute + GEMM round trip per gate.  Gate
+values never leave the device.
 """
 
 from __future__ import annotations
