@@ -151,15 +151,18 @@ int tnc_contract_split(const tnc_plan* plan, int32_t blocks, int32_t group, cons
  * Reference semantics of contract_pair(T, G) (contract.py:149-165): the two
  * contracted legs are removed and the gate's out legs are appended at the end.
  * The output is written in the final leg order after all gates; t_out must
- * not alias t_in.  Workspace (tnc_absorb_chain_workspace): the group unitary
- * table, plus one tensor-sized buffer when the chain needs more than one HBM
- * pass.  The gate values stay on the device (no host round trip, no sync). */
+ * not alias t_in.  Workspace (tnc_absorb_chain_workspace): the oriented gate
+ * table (256 B per gate), plus one tensor-sized buffer when the chain needs
+ * more than one HBM pass.  The gate values stay on the device (no host round
+ * trip, no sync): each pass's table is copied device-to-device, on the
+ * caller's stream, into the library's per-device constant bank; chains
+ * launched on different streams are ordered by an event on that bank. */
 int tnc_absorb_chain(int32_t t_rank, const void* t_in, void* t_out, int32_t n_gates,
                      const void* const* gates, const int64_t* gate_strides, const int32_t* axes,
                      void* workspace, size_t workspace_bytes, void* stream);
 int tnc_absorb_chain_workspace(int32_t t_rank, int32_t n_gates, const int32_t* axes,
                                size_t* workspace_bytes);
-/* HBM passes and 3-axis gate groups the planner uses for this chain. */
+/* HBM passes and (<= 5-axis) gate groups the planner uses for this chain. */
 int tnc_absorb_chain_info(int32_t t_rank, int32_t n_gates, const int32_t* axes, int32_t* passes,
                           int32_t* groups);
 
