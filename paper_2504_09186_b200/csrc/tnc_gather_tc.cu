@@ -214,8 +214,8 @@ struct GtCursor {
   }
 };
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
-__global__ void __launch_bounds__(kGtThreads, 1) gather_tc_kernel(const __grid_constant__ GtParams p) {
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC>
+__global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid_constant__ GtParams p) {
   using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
@@ -559,7 +559,7 @@ struct GatherTcPlan {
   GtParams p;
   GtParams p2;              // paired layout (16-byte K pairs), when pair_x
   bool pair_x = false, pair_y = false;
-  int nmma = 0, kbc = 0;
+  int nmma = 0, kbc = 0, occ = 1;  // occ: CTAs per SM (2 on the narrowest tiles)
   int64_t rows_x = 0, rows_y = 0, k = 0;
   std::vector<int64_t> tabs_host;
   mutable int64_t* tabs_dev = nullptr;
@@ -635,7 +635,12 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   if (fx < 6) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: X has fewer than 64 rows");
   const int nmma = std::max(32, 2 << fy);
   const int lgn = nmma == 32 ? 4 : nmma == 64 ? 5 : nmma == 128 ? 6 : 7;  // log2(nmma / 2)
-  const int kbc = nmma <= 64 ? 32 : 16;
+  // narrowest tiles (<= 16 Y columns): 16-K k-blocks and two CTAs per SM -- the
+  // loop is a latency chain, and a second CTA hides it where more bytes in
+  // flight per CTA did not
+  const char* occ_s = std::getenv("TNC_GT_OCC2");
+  const int occ = (nmma == 32 && !(occ_s && std::atoi(occ_s) == 0)) ? 2 : 1;
+  const int kbc = (nmma <= 64 && occ == 1) ? 32 : 16;
   const int kb = kbc == 32 ? 5 : 4;
   if (c < kb) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: K smaller than one k-block");
   const int rb = std::min(7, fx);
@@ -923,6 +928,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   GtParams& p = plan->p;
   plan->nmma = nmma;
   plan->kbc = kbc;
+  plan->occ = occ;
   plan->rows_x = int64_t{1} << fx;
   plan->rows_y = int64_t{1} << fy;
   plan->k = int64_t{1} << c;
@@ -966,7 +972,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   carry_deltas(som, p.dom);
   carry_deltas(scm, p.dcm);
   // k-splits: enough units for every SM, each SM's share within ~3% of the others
-  const int sms = num_sms();
+  const int sms = num_sms() * occ;
   int splits = 1;
   if (p.m_blocks < 4 * sms) {
     double best_eff = 0;
@@ -993,7 +999,7 @@ int gather_tc_prepare(int n_legs, const GatherTcLeg* legs, GatherTcPlan** out) {
   // the operand pointers are 16-byte aligned.
   const bool px = legs[xt[0]].kind == 1 && legs[xt[0]].x_stride == 1;
   // (not for 256-column tiles: the paired Y registers spill there, measured slower)
-  const bool py = px && nmma <= 128 && yt[0] == xt[0] && legs[yt[0]].y_stride == 1;
+  const bool py = px && nmma <= 128 && occ == 1 && yt[0] == xt[0] && legs[yt[0]].y_stride == 1;
   const char* pair_env = std::getenv("TNC_GT_PAIR");
   if (px && !(pair_env && std::atoi(pair_env) == 0)) {
     plan->p2 = p;
@@ -1017,12 +1023,12 @@ void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
 
 namespace {
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY>
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC>
 int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
   using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
-  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY, OCC>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
-  const int grid = static_cast<int>(std::min<int64_t>(units, num_sms()));
+  const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(num_sms()) * OCC));
   ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
   kern<<<grid, kGtThreads, Cfg::kSmem, stream>>>(p);
   TNC_CHECK_LAUNCH();
@@ -1050,19 +1056,24 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
   const double M = static_cast<double>(plan->rows_x), N = static_cast<double>(plan->rows_y),
                K = static_cast<double>(plan->k);
   const double flops = 8.0 * M * N * K, bytes = 8.0 * (M * K + N * K + M * N);
-#define TNC_GT_MODES(N, KBC, ST)                                                        \
-  do {                                                                                  \
-    if (py) return launch_gt<N, KBC, ST, true, true>(p, units, flops, bytes, stream);   \
-    if (px) return launch_gt<N, KBC, ST, true, false>(p, units, flops, bytes, stream);  \
-    return launch_gt<N, KBC, ST, false, false>(p, units, flops, bytes, stream);         \
+#define TNC_GT_MODES(N, KBC, ST)                                                           \
+  do {                                                                                     \
+    if (py) return launch_gt<N, KBC, ST, true, true, 1>(p, units, flops, bytes, stream);   \
+    if (px) return launch_gt<N, KBC, ST, true, false, 1>(p, units, flops, bytes, stream);  \
+    return launch_gt<N, KBC, ST, false, false, 1>(p, units, flops, bytes, stream);         \
   } while (0)
   switch (plan->nmma) {
-    case 32: TNC_GT_MODES(32, 32, 2);
+    case 32:
+      if (plan->occ == 2) {  // (a memory-paired Y would leave fewer Y elements than threads)
+        if (px) return launch_gt<32, 16, 2, true, false, 2>(p, units, flops, bytes, stream);
+        return launch_gt<32, 16, 2, false, false, 2>(p, units, flops, bytes, stream);
+      }
+      TNC_GT_MODES(32, 32, 2);
     case 64: TNC_GT_MODES(64, 32, 2);
     case 128: TNC_GT_MODES(128, 16, 3);
     case 256:
-      if (px) return launch_gt<256, 16, 2, true, false>(p, units, flops, bytes, stream);
-      return launch_gt<256, 16, 2, false, false>(p, units, flops, bytes, stream);
+      if (px) return launch_gt<256, 16, 2, true, false, 1>(p, units, flops, bytes, stream);
+      return launch_gt<256, 16, 2, false, false, 1>(p, units, flops, bytes, stream);
     default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
   }
 #undef TNC_GT_MODES
