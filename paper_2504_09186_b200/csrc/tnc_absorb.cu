@@ -75,11 +75,14 @@ constexpr int kMemThrBits = 7;
 constexpr int kCubeBits = 5;
 constexpr int kCube = 1 << kCubeBits;
 constexpr int kMaxGroups = 24;                // groups per pass
-constexpr int kMaxPassGates = 64;             // gates per pass (constant bank: 256 B each)
+constexpr int kMaxPassGates = 64;             // gates per pass (constant bank: 192 B each)
 constexpr int kMaxChainGates = 512;
 
-// The running pass's gate coefficients U[o][i] as (re, -im, im, 0), gate-major.
-__constant__ float4 c_gates[kMaxPassGates * 16];
+// The running pass's gate coefficients, 48 floats per gate: 16 aligned pairs
+// (-im, im) of U[o][i], then the 16 real parts (an FFMA2 takes the pair as a
+// 64-bit uniform-register operand and the real part as a broadcast scalar).
+constexpr int kGateFloats = 48;
+__constant__ float c_gates[kMaxPassGates * kGateFloats];
 
 struct GroupParams {
   int cube_slot[kCubeBits];  // slot vectors of the cube (register-index) bits
@@ -110,8 +113,8 @@ struct AbsorbParams {
   int64_t outer_out[TNC_MAX_RANK];
 };
 
-// Device gate tables: entry j = 16 float4 (U[o][i] as (re, -im, im, 0)) of
-// chain gate src[j], oriented so that its in_a axis is the lower cube bit.
+// Device gate tables: entry j = the 48 floats (see c_gates) of chain gate
+// src[j], oriented so that its in_a axis is the lower cube bit.
 struct TableParams {
   int n;
   short src[kMaxChainGates];
@@ -162,7 +165,7 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
 // half swaps are operand modifiers -- no moves, no negations:
 //   acc += (u.re, u.re) * (x.re, x.im) + (-u.im, u.im) * (x.im, x.re)
 template <int LA, int LB>
-__device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* u) {
+__device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float* u) {
 #pragma unroll
   for (int s = 0; s < kCube; ++s) {
     if ((s >> LA) & 1) continue;
@@ -179,16 +182,16 @@ __device__ __forceinline__ void apply_local(float2 (&v)[kCube], const float4* u)
       u64 acc = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float4 c = u[o * 4 + i];
-        acc = ffma2(bcast(c.x), x[i], acc);
-        acc = ffma2(as_u64(make_float2(c.y, c.z)), xs[i], acc);
+        const float2 ci = reinterpret_cast<const float2*>(u)[o * 4 + i];
+        acc = ffma2(bcast(u[32 + o * 4 + i]), x[i], acc);
+        acc = ffma2(as_u64(ci), xs[i], acc);
       }
       v[idx[o]] = as_f2(acc);
     }
   }
 }
 
-__device__ __forceinline__ void apply_gate(float2 (&v)[kCube], int local, const float4* u) {
+__device__ __forceinline__ void apply_gate(float2 (&v)[kCube], int local, const float* u) {
   switch (local) {
     case 8 * 0 + 1: apply_local<0, 1>(v, u); break;
     case 8 * 0 + 2: apply_local<0, 2>(v, u); break;
@@ -205,7 +208,7 @@ __device__ __forceinline__ void apply_gate(float2 (&v)[kCube], int local, const 
 }
 
 // Gate tables from the caller's device gate tensors (one thread per entry).
-__global__ void absorb_table_kernel(const TableParams p, float4* __restrict__ table) {
+__global__ void absorb_table_kernel(const TableParams p, float* __restrict__ table) {
   const int j = blockIdx.x;
   const int e = threadIdx.x;  // 16 entries
   if (j >= p.n || e >= 16) return;
@@ -215,7 +218,10 @@ __global__ void absorb_table_kernel(const TableParams p, float4* __restrict__ ta
   const int oo = q(o), ii = q(i);
   const int64_t* st = p.gstride[g];
   const float2 u = p.gate[g][(oo >> 1) * st[0] + (oo & 1) * st[1] + (ii >> 1) * st[2] + (ii & 1) * st[3]];
-  table[16 * j + e] = make_float4(u.x, -u.y, u.y, 0.f);
+  float* g_out = table + kGateFloats * j;
+  g_out[2 * e] = -u.y;
+  g_out[2 * e + 1] = u.y;
+  g_out[32 + e] = u.x;
 }
 
 // Sum over the outer (non-tile) axes of tile t: one warp, lanes split the axes.
@@ -320,12 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
       if (t >= p.n_tiles) break;
       const int b = static_cast<int>(k % kBufs);
       mbar_wait(&full[b], static_cast<uint32_t>((k / kBufs) & 1));
-      char* tile_b = reinterpret_cast<char*>(tiles + b * kTile);
+      // the buffer's byte offset (a multiple of 64 KB) rides in the running XOR
+      // with the in-tile offsets, so an element address is one LOP3
+      char* tile_b = reinterpret_cast<char*>(tiles);
+      const uint32_t buf_off = static_cast<uint32_t>(b) * (kTile * 8u);
       for (int g = 0; g < p.n_groups; ++g) {
         const GroupParams& gp = p.g[g];
         // byte offsets inside the tile buffer: the running XOR is the whole
         // per-element address arithmetic (the buffer base is uniform)
-        uint32_t base = 0;
+        uint32_t base = buf_off;
 #pragma unroll
         for (int j = 0; j < 5; ++j)
           if ((lane >> j) & 1) base ^= static_cast<uint32_t>(gp.lane_slot[j]) << 3;
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) absorb_pass_kernel(const float2* 
           if (n > 0) a ^= sb[ctz5(n)];
           c[n ^ (n >> 1)] = *reinterpret_cast<const float2*>(tile_b + a);
         }
-        for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], c_gates + 16 * k2);
+        for (int k2 = gp.g_first; k2 < gp.g_last; ++k2) apply_gate(c, p.gate_local[k2], c_gates + kGateFloats * k2);
         asm volatile("mov.b32 %0, %1;" : "=r"(a) : "r"(base));  // recompute, do not keep, the addresses
 #pragma unroll
         for (int n = 0; n < kCube; ++n) {
@@ -731,8 +740,10 @@ int plan_chain(int r, int n_gates, const int32_t* axes, ChainPlan& cp) {
   return TNC_OK;
 }
 
-// gate tables: 16 float4 per gate
-size_t table_bytes(int n_gates) { return (static_cast<size_t>(std::max(n_gates, 1)) * 256 + 255) & ~size_t(255); }
+// gate tables: 48 floats per gate
+size_t table_bytes(int n_gates) {
+  return (static_cast<size_t>(std::max(n_gates, 1)) * kGateFloats * sizeof(float) + 255) & ~size_t(255);
+}
 
 // c_gates is one per device: chains launched on different streams take turns
 // (the later stream waits for the earlier chain's last pass).
@@ -767,7 +778,7 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
   for (int g = 0; g < n_gates; ++g)
     if (gates[g] == nullptr) TNC_RET(TNC_ERR_INVALID, "absorb: null gate pointer");
   float2* ws = static_cast<float2*>(workspace);
-  float4* table = reinterpret_cast<float4*>(static_cast<uint8_t*>(workspace) + tensor);
+  float* table = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + tensor);
 
   std::vector<AbsorbParams> params(P);
   TableParams tp;
@@ -809,8 +820,8 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
     const AbsorbParams& p = params[k];
     const int64_t blocks = std::min<int64_t>(p.n_tiles, static_cast<int64_t>(num_sms()));
     if (p.n_gates > 0)
-      TNC_CUDA_TRY(cudaMemcpyToSymbolAsync(c_gates, table + 16 * p.table_base,
-                                           static_cast<size_t>(p.n_gates) * 16 * sizeof(float4), 0,
+      TNC_CUDA_TRY(cudaMemcpyToSymbolAsync(c_gates, table + kGateFloats * p.table_base,
+                                           static_cast<size_t>(p.n_gates) * kGateFloats * sizeof(float), 0,
                                            cudaMemcpyDeviceToDevice, stream));
     {
       // algorithmic work: 16 complex MACs (64 real flops) per 4 elements per gate
