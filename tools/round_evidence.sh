@@ -1,4 +1,4 @@
-# round-2 evidence: GPU suite, one bench line per BASELINE config, the 3xTF32 C3 line, the reference arm
+# round evidence (usage: bash tools/round_evidence.sh): GPU suite, one bench line per BASELINE config, the 3xTF32 C3 line, the reference arm
 mkdir -p gpurun_out
 (timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r02_gputest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02_gputest.log)
 timeout 600 python bench.py --workload c1 --steps 10 --warmup 3 > gpurun_out/r02_bench_c1.jsonl 2> gpurun_out/r02_bench_c1.err; echo "c1 rc=$?"
