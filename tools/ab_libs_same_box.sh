@@ -1,4 +1,4 @@
-# same-box A/B of prebuilt library variants on C1: usage s4_ab_libs.sh lib1.so lib2.so ...
+# same-box A/B of prebuilt library variants on C1: usage: bash tools/ab_libs_same_box.sh lib1.so lib2.so ...
 L=paper_2504_09186_b200/libtnc_b200.so
 cp $L /tmp/new.so
 for lib in "$@"; do
