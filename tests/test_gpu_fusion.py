@@ -151,3 +151,32 @@ def test_executor_fuses_stem_chain(cuda_ready, monkeypatch):
     monkeypatch.setenv("TNC_FUSE_ABSORB", "0")
     plain = run_open(net, tree)
     assert rel_l2(plain.numpy(), got.numpy()) <= 1e-5
+
+
+def test_absorb_chains_on_two_streams_share_the_constant_bank(cuda_ready):
+    """Each pass's gate coefficients live in one per-device constant table;
+    chains launched on different streams must take turns on it (an event
+    orders the later stream behind the earlier chain's last pass).  Two
+    multi-pass chains with different gates are interleaved on two side
+    streams several times; each result must still equal its own oracle."""
+    from paper_2504_09186_b200.fusion import absorb_chain
+
+    cases = []
+    for rank, n_gates, seed in ((21, 24, 11), (20, 30, 12)):
+        t_labels, data, gates, t, gs = _chain(rank, n_gates, seed)
+        ref = (tuple(t_labels), (2,) * rank, data.astype(np.complex128))
+        for ia, ib, oa, ob, u in gates:
+            ref = tncref.contract(ref, ((oa, ob, ia, ib), (2, 2, 2, 2), u.astype(np.complex128)))
+        cases.append((t, gs, ref))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = [[], []]
+    for _ in range(4):
+        for i, (t, gs, _) in enumerate(cases):
+            with torch.cuda.stream(streams[i]):
+                outs[i].append(absorb_chain(t, gs))
+    torch.cuda.synchronize()
+    for i, (_, _, ref) in enumerate(cases):
+        for got in outs[i]:
+            assert list(got.labels) == list(ref[0])
+            assert rel_l2(got.numpy(), ref[2]) <= 1e-5
