@@ -126,8 +126,15 @@ struct tnc_plan {
   int64_t g_chunks = 1;
   std::vector<int64_t> g_host;
   mutable int64_t* g_dev = nullptr;
+  // tensor-core GEMM writing the caller's leg order itself: offset of C[x, y] =
+  // out_tab[x] + out_tab[rows_x + y] (the order permutes row legs and column
+  // legs, so the offset separates); uploaded once per plan
+  bool fuse_out = false;
+  std::vector<int64_t> out_tab_host;
+  mutable int64_t* out_tab_dev = nullptr;
   ~tnc_plan() {
     if (g_dev) cudaFree(g_dev);
+    if (out_tab_dev) cudaFree(out_tab_dev);
     if (stream) tnc::stream_destroy(stream);
     if (gt) tnc::gather_tc_destroy(gt);
   }
@@ -687,6 +694,36 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
       if (forced >= 1) p->k_splits = static_cast<int32_t>(std::min<int64_t>(forced, kblocks));
     }
   }
+  // K2 with one split writes a custom output order from its epilogue (no
+  // temporary, no output permutation pass): per-row and per-column offsets
+  if (p->custom_out && tc && p->k_splits == 1 && p->rows_x + p->rows_y <= (int64_t{1} << 22) &&
+      env_flag("TNC_FUSE_OUT", 1) && !(std::getenv("TNC_TC_CFG") && std::atoi(std::getenv("TNC_TC_CFG")) == 2)) {
+    const auto outs = final_out_strides(p, free_a, free_b);
+    auto stride_of = [&](int32_t label) {
+      for (const auto& e : outs)
+        if (e.first == label) return e.second;
+      return int64_t{0};
+    };
+    auto fill = [&](const std::vector<Leg>& legs, int64_t rows, int64_t* dst) {
+      // row-major over the legs, last leg fastest
+      for (int64_t r = 0; r < rows; ++r) {
+        int64_t rem = r, off = 0;
+        for (int i = static_cast<int>(legs.size()) - 1; i >= 0; --i) {
+          off += (rem % legs[i].dim) * stride_of(legs[i].label);
+          rem /= legs[i].dim;
+        }
+        dst[r] = off;
+      }
+    };
+    p->out_tab_host.assign(static_cast<size_t>(p->rows_x + p->rows_y), 0);
+    fill(X.free, p->rows_x, p->out_tab_host.data());
+    fill(Y.free, p->rows_y, p->out_tab_host.data() + p->rows_x);
+    if (upload_table(p->out_tab_host.data(), p->out_tab_host.size(), &p->out_tab_dev) != TNC_OK) {
+      delete p;
+      return TNC_ERR_CUDA;
+    }
+    p->fuse_out = true;
+  }
   // workspace
   const size_t eb = elem_bytes(p->dtype);
   const bool kernel_gathers = want == TNC_VARIANT_TCGATHER;  // operands read in place
@@ -712,7 +749,7 @@ int tnc_plan_contract(const tnc_tensor_desc* a, const tnc_tensor_desc* b, int32_
     off = align_up(off + static_cast<size_t>(chunks) * m * n * eb);
   }
   p->off_tmp = off;
-  if (p->custom_out && !(kernel_gathers && gather_tc_splits(p->gt) == 1))
+  if (p->custom_out && !p->fuse_out && !(kernel_gathers && gather_tc_splits(p->gt) == 1))
     off = align_up(off + static_cast<size_t>(m) * n * eb);
   p->ws_bytes = off;
   p->ws_layout = off;
@@ -796,7 +833,8 @@ static bool fused_gather_split(const tnc_plan* p, const Operand& op, const void*
 
 static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* ym, int64_t ldy,
                     void* c, int64_t ldcm, int64_t ldcn, uint8_t* ws, int k_splits,
-                    cudaStream_t st, bool x_planes_done = false, bool y_planes_done = false) {
+                    cudaStream_t st, bool x_planes_done = false, bool y_planes_done = false,
+                    const int64_t* row_off = nullptr, const int64_t* col_off = nullptr) {
   if (p->variant == TNC_VARIANT_TC3XTF32 || p->variant == TNC_VARIANT_TC3XF16) {
     const bool f16 = p->variant == TNC_VARIANT_TC3XF16;
     const size_t pe = f16 ? 2 : 4;
@@ -818,7 +856,7 @@ static int run_gemm(const tnc_plan* p, const void* xm, int64_t ldx, const void* 
     }
     return tc_cgemm_launch(f16 ? 1 : 0, p->rows_x, p->rows_y, p->k, p->kp, ab, as, bb, bs,
                            f16 ? ex : nullptr, f16 ? ey : nullptr, c, ldcm, ldcn, k_splits,
-                           reinterpret_cast<float*>(ws + p->off_partials), st);
+                           reinterpret_cast<float*>(ws + p->off_partials), st, row_off, col_off);
   }
   if (p->variant == TNC_VARIANT_SPLITK && p->gather_splitk) {
     if (!p->g_dev) TNC_RET(TNC_ERR_INVALID, "split-K gather: plan tables missing");
@@ -865,6 +903,11 @@ int tnc_contract(const tnc_plan* p, const void* a, const void* b, void* c, void*
   }
   if (!x_done) TNC_TRY(prep_operand(p, p->x, xsrc, ws, p->off_x, &xm, &ldx, st));
   if (!y_done) TNC_TRY(prep_operand(p, p->y, ysrc, ws, p->off_y, &ym, &ldy, st));
+  if (p->fuse_out) {
+    if (!p->out_tab_dev) TNC_RET(TNC_ERR_INVALID, "contract: plan output tables missing");
+    return run_gemm(p, xm, ldx, ym, ldy, c, p->ldcm, p->ldcn, ws, p->k_splits, st, x_done, y_done,
+                    p->out_tab_dev, p->out_tab_dev + p->rows_x);
+  }
   void* dst = p->custom_out ? static_cast<void*>(ws + p->off_tmp) : c;
   TNC_TRY(run_gemm(p, xm, ldx, ym, ldy, dst, p->ldcm, p->ldcn, ws, p->k_splits, st, x_done, y_done));
   if (p->custom_out) {

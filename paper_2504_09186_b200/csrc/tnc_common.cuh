@@ -183,7 +183,8 @@ int f16_split_launch(int mode, int64_t R, int64_t K, int64_t Kp, const void* X, 
 int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Abig,
                     const void* Asmall, const void* Bbig, const void* Bsmall, const int* ex,
                     const int* ey, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
-                    float* partials, cudaStream_t stream);
+                    float* partials, cudaStream_t stream,
+                    const int64_t* row_off = nullptr, const int64_t* col_off = nullptr);
 // fixed-order pairwise tree reduction of P partial [M,N] fp32-complex buffers
 int tree_reduce_launch(int dtype, int64_t P, int64_t MN, void* partials, void* out_or_null,
                        int64_t M, int64_t N, int64_t ldcm, int64_t ldcn, cudaStream_t stream);

@@ -133,6 +133,11 @@ struct TcParams {
   float2* partials;      // [splits][M][N] when splits > 1
   const int* ex;         // 3xFP16: per-row scale exponent of A (nullptr for TF32)
   const int* ey;         // 3xFP16: per-complex-column scale exponent of B
+  // fused output permutation (one split): C[row_off[m] + col_off[n]] -- the
+  // caller's leg order is a permutation of the row legs and the column legs,
+  // so the offset of C[m, n] separates into a row part and a column part
+  const int64_t* row_off;
+  const int64_t* col_off;
 };
 
 // Undo the 3xFP16 per-row / per-column power-of-two operand scaling of one
@@ -371,7 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float2* drow = dst + row * sm;
         if constexpr (F16) unscale<Cfg::kHalf>(acc, p, row, ncol0);
-        if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
+        if (p.col_off != nullptr && p.splits == 1) {
+          float2* prow = p.C + p.row_off[row];
+#pragma unroll
+          for (int j = 0; j < Cfg::kHalf / 2; ++j) {
+            const int64_t n = ncol0 + j;
+            if (n < p.N) prow[__ldg(p.col_off + n)] = make_float2(acc[2 * j], acc[2 * j + 1]);
+          }
+        } else if (sn == 1 && (sm % 2) == 0 && ncol0 + Cfg::kHalf / 2 <= p.N) {
           float4* d4 = reinterpret_cast<float4*>(drow + ncol0);
 #pragma unroll
           for (int j = 0; j < Cfg::kHalf / 4; ++j)
@@ -724,7 +736,8 @@ int env_int(const char* name, int dflt) {
 template <int BN, int SWZ, int STAGES, bool F16>
 int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, const void* As,
                const void* Bb, const void* Bs, const int* ex, const int* ey, void* C, int64_t ldcm,
-               int64_t ldcn, int k_splits, float* partials, cudaStream_t stream) {
+               int64_t ldcn, int k_splits, float* partials, cudaStream_t stream,
+               const int64_t* row_off = nullptr, const int64_t* col_off = nullptr) {
   using Cfg = TcCfg<BN, SWZ, STAGES, F16>;
   const int64_t Kr = 2 * Kp;
   CUtensorMap mAb, mAs, mBb, mBs;
@@ -754,6 +767,9 @@ int launch_cfg(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, cons
   p.partials = p.splits > 1 ? reinterpret_cast<float2*>(partials) : nullptr;
   p.ex = ex;
   p.ey = ey;
+  if (row_off && p.splits != 1) TNC_RET(TNC_ERR_INVALID, "tc_cgemm: fused output order needs one split");
+  p.row_off = row_off;
+  p.col_off = col_off;
   const int64_t units = static_cast<int64_t>(p.m_blocks) * p.n_blocks * p.splits;
   if (units > INT32_MAX) TNC_RET(TNC_ERR_UNSUPPORTED, "tc_cgemm: too many tiles");
   auto kern = tc_cgemm_kernel<BN, SWZ, STAGES, F16>;
@@ -821,27 +837,29 @@ int launch_cfg_2sm(int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Ab, 
 int tc_cgemm_launch(int f16, int64_t M, int64_t N, int64_t K, int64_t Kp, const void* Abig,
                     const void* Asmall, const void* Bbig, const void* Bsmall, const int* ex,
                     const int* ey, void* C, int64_t ldcm, int64_t ldcn, int k_splits,
-                    float* partials, cudaStream_t stream) {
+                    float* partials, cudaStream_t stream, const int64_t* row_off, const int64_t* col_off) {
   if (M <= 0 || N <= 0) return TNC_OK;
   if (Kp % (f16 ? 32 : 16) != 0)
     TNC_RET(TNC_ERR_INVALID, "tc_cgemm: Kp must be a multiple of 32 (f16) / 16 (tf32)");
   const int cfg = env_int("TNC_TC_CFG", 0);
 #define TNC_TC_ARGS M, N, K, Kp, Abig, Asmall, Bbig, Bsmall, ex, ey, C, ldcm, ldcn, k_splits, partials, stream
+#define TNC_TC_ARGS_OUT TNC_TC_ARGS, row_off, col_off
   if (f16) {
     if (2 * N >= 256) {
-      if (cfg == 1) return launch_cfg<256, 64, 4, true>(TNC_TC_ARGS);
+      if (cfg == 1) return launch_cfg<256, 64, 4, true>(TNC_TC_ARGS_OUT);
       // the 2-CTA kernel (cfg 2) wins on square 8192^3 but loses on the C3
       // step shapes; the 1-SM kernel is the default until that is understood
-      if (cfg == 2 && M >= 256) return launch_cfg_2sm<256, 128, 3, true>(TNC_TC_ARGS);
-      return launch_cfg<256, 128, 2, true>(TNC_TC_ARGS);
+      if (cfg == 2 && M >= 256 && !row_off) return launch_cfg_2sm<256, 128, 3, true>(TNC_TC_ARGS);
+      return launch_cfg<256, 128, 2, true>(TNC_TC_ARGS_OUT);
     }
-    return launch_cfg<128, 128, 3, true>(TNC_TC_ARGS);
+    return launch_cfg<128, 128, 3, true>(TNC_TC_ARGS_OUT);
   }
   if (2 * N >= 256) {
-    if (cfg == 1) return launch_cfg<256, 128, 2, false>(TNC_TC_ARGS);
-    return launch_cfg<256, 64, 4, false>(TNC_TC_ARGS);
+    if (cfg == 1) return launch_cfg<256, 128, 2, false>(TNC_TC_ARGS_OUT);
+    return launch_cfg<256, 64, 4, false>(TNC_TC_ARGS_OUT);
   }
-  return launch_cfg<128, 64, 6, false>(TNC_TC_ARGS);
+  return launch_cfg<128, 64, 6, false>(TNC_TC_ARGS_OUT);
+#undef TNC_TC_ARGS_OUT
 #undef TNC_TC_ARGS
 }
 

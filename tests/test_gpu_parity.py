@@ -468,3 +468,30 @@ def test_fused_gather_split_bitwise(cuda_ready, seed, monkeypatch):
     want = tncref.contract((tuple(la), (2,) * len(la), da.astype(np.complex128)),
                            (tuple(lb), (2,) * len(lb), db.astype(np.complex128)))
     assert rel_l2(fused, want[2]) <= TOL_C64
+
+
+@pytest.mark.parametrize("variant_name", ["VARIANT_TC3XF16", "VARIANT_TC3XTF32"])
+@pytest.mark.parametrize("fa,fb,nc,seed", [(9, 8, 7, 0), (7, 10, 6, 1), (8, 8, 9, 2), (11, 7, 5, 3)])
+def test_tensor_core_gemm_writes_custom_output_order(cuda_ready, variant_name, fa, fb, nc, seed):
+    """K2 with one split writes the caller's leg order from its epilogue
+    (row / column offset tables built at plan time): random output orders,
+    either operand the larger one, vs the oracle's contract + permute
+    (reference contract.py:149-165, tensor.py:252-274)."""
+    from paper_2504_09186_b200 import DenseTensor, Index, _lib, contract_pair
+
+    rng = np.random.default_rng(100 + seed)
+    la = [f"a{i}" for i in range(fa)] + [f"k{i}" for i in range(nc)]
+    lb = [f"k{i}" for i in range(nc)] + [f"b{i}" for i in range(fb)]
+    rng.shuffle(la)
+    rng.shuffle(lb)
+    da = (rng.standard_normal(2 ** len(la)) + 1j * rng.standard_normal(2 ** len(la))).astype(np.complex64)
+    db = (rng.standard_normal(2 ** len(lb)) + 1j * rng.standard_normal(2 ** len(lb))).astype(np.complex64)
+    free = [l for l in la if l.startswith("a")] + [l for l in lb if l.startswith("b")]
+    out = list(rng.permutation(free))
+    got = contract_pair(DenseTensor([Index(l) for l in la], da), DenseTensor([Index(l) for l in lb], db),
+                        out_order=[Index(l) for l in out], variant=getattr(_lib, variant_name))
+    ref = tncref.contract((tuple(la), (2,) * len(la), da.astype(np.complex128)),
+                          (tuple(lb), (2,) * len(lb), db.astype(np.complex128)))
+    ref = tncref.permute(ref, out)
+    assert [ix.label for ix in got.indices] == out
+    assert rel_l2(got.numpy(), ref[2]) <= TOL_C64
