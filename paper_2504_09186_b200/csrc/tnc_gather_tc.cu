@@ -345,9 +345,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
 
   using XT = typename Cfg::XT;
   using YT = typename Cfg::YT;
-  // 64-row operands: the phantom row bit is the tile's top bit, the thread's
-  // top iteration bit, so the upper half of its elements does not exist
-  const int x_iters = Cfg::kXPer >> (7 - p.rbits);
   XT cx[Cfg::kXPer];
   YT cy[Cfg::kYPer];
   auto load = [&](XT (&vx)[Cfg::kXPer], YT (&vy)[Cfg::kYPer]) {
@@ -355,7 +352,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
     const float2* yb = p.Y + yk_off;
 #pragma unroll
     for (int i = 0; i < Cfg::kXPer; ++i) {
-      if (i >= x_iters) continue;  // phantom rows (the top iteration bits): nothing to load
       if constexpr (PX) vx[i] = ldg_stream4(xb + xoff(i));
       else vx[i] = ldg_stream(xb + xoff(i));
     }
@@ -443,7 +439,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
       const uint32_t st = smem0 + s * Cfg::kStage;
 #pragma unroll
       for (int i = 0; i < Cfg::kXPer; ++i) {
-        if (i >= x_iters) continue;  // phantom rows: their smem (and TMEM lanes) are never read back
         const uint32_t a = st + xadr(i);
         if constexpr (PX) {  // (k, k + 1) pair: 16 contiguous bytes per plane
           const float r0 = tf32_hi(cx[i].x), i0 = tf32_hi(cx[i].y), r1 = tf32_hi(cx[i].z), i1 = tf32_hi(cx[i].w);
