@@ -214,8 +214,14 @@ struct GtCursor {
   }
 };
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC>
-__global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid_constant__ GtParams p) {
+// MW (256-column tiles): a third warpgroup holds a dedicated MMA-issue warp.
+// A clock64 trace showed warp 0 spending a third of every k-block inside the
+// MMA issue (the issue blocks while the tensor pipe works through the queue)
+// while the other seven workers waited half of theirs for the stage that only
+// warp 0's late issue would release.  The block launches with 384 threads x
+// 168 registers; the MMA warpgroup drops to 24 and the workers rise to 240.
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC, bool MW = false>
+__global__ void __launch_bounds__(MW ? kGtThreads + 128 : kGtThreads, OCC) gather_tc_kernel(const __grid_constant__ GtParams p) {
   using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
@@ -268,6 +274,59 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
   const uint32_t tmem_base = tmem_slot;
   const uint32_t smem0 = smem_u32(smem);
 
+  // Barrier waits use the suspend-hinted try_wait: polling without the hint
+  // (tried on the round-1 verdict's advice) measured 2-3 % slower on C1a / C1c,
+  // and a run-time switch between the two cost another 3-7 % in registers.
+  auto wait = [&](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
+
+  GtCursor ic;  // MMA issue (warp 0, or the MMA warp)
+  ic.init(p, units);
+  int i_in_chunk = 0;
+  uint32_t i_ch = 0, i_g = 0, dcol = 0;
+  // MMAs of the issue cursor's k-block (staged as k-block i_g): one elected lane
+  auto issue_kblock = [&]() {
+    if (i_in_chunk == 0) {
+      const uint32_t b = i_ch & 1;
+      wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
+      fence_after_sync();
+      dcol = tmem_base + b * NMMA;
+    }
+    const uint32_t s = i_g % STAGES;
+    wait(&full[s], (i_g / STAGES) & 1);
+    fence_after_sync();
+    const uint32_t st = smem0 + s * Cfg::kStage;
+#pragma unroll
+    for (int a = 0; a < Cfg::kAtoms; ++a) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t xs = st + a * Cfg::kXAtom + kk * 32;
+        const uint32_t ys = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
+        const uint64_t x_big = umma_desc_sw128(xs);
+        const uint64_t x_small = umma_desc_sw128(xs + Cfg::kXPlane);
+        const uint64_t y_big = umma_desc_sw128(ys);
+        const uint64_t y_small = umma_desc_sw128(ys + Cfg::kYPlane);
+        const uint32_t acc0 = (i_in_chunk > 0 || a > 0 || kk > 0) ? 1u : 0u;
+        // small products first: accumulated before the big one
+        mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
+        mma_tf32_elect(dcol, x_big, y_small, Cfg::kIdesc, 1u);
+        mma_tf32_elect(dcol, x_big, y_big, Cfg::kIdesc, 1u);
+      }
+    }
+    mma_commit_elect(&empty[s]);
+    ++i_g;
+    const bool unit_end = ic.kb + 1 == ic.kb_hi;
+    if (++i_in_chunk == p.chunk_kb || unit_end) {
+      mma_commit_elect(&tfull[i_ch & 1]);
+      ++i_ch;
+      i_in_chunk = 0;
+    }
+    ic.next(p);
+  };
+
+  // Everything a worker warp does (gather, split, stage, fold, store); a lambda
+  // so that, with a dedicated MMA warp, it sits inside the branch that starts
+  // with the workers' setmaxnreg (ptxas allocates registers per such region).
+  auto worker_body = [&]() {
   const int quad = warp & 3;
   const int half = warp >> 2;
   uint32_t xg_lo = 0, yg_lo = 0, xs_lo = 0, ys_lo = 0;
@@ -315,11 +374,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
   float acc[Cfg::kHalf];
 #pragma unroll
   for (int j = 0; j < Cfg::kHalf; ++j) acc[j] = 0.f;
-  // Barrier waits use the suspend-hinted try_wait: polling without the hint
-  // (tried on the round-1 verdict's advice) measured 2-3 % slower on C1a / C1c,
-  // and a run-time switch between the two cost another 3-7 % in registers.
-  auto wait = [&](uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); };
-
   GtCursor pc;  // loads (one k-block ahead of the smem stores)
   pc.init(p, units);
   // operand offsets of the load cursor's k-block
@@ -330,10 +384,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
     yk_off = pc.kb == 0 ? 0 : tab4(p.tabs + 4 * 1024, pc.kb);
   };
   open_k();
-  GtCursor ic;  // MMA issue (warp 0)
-  ic.init(p, units);
-  int i_in_chunk = 0;
-  uint32_t i_ch = 0, i_g = 0, dcol = 0;
   GtCursor fc;  // fold: this CTA's chunk sequence
   fc.init(p, units);
   // final-output (one split) or partial-layout offset of the fold cursor's m-block
@@ -381,45 +431,6 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
   //      behind them); once nothing is left to stage, fold everything
   // A chunk's TMEM buffer is folded (step 4) an iteration before the MMAs
   // that reuse it are issued (step 2), so no step waits on a later one.
-  // MMAs of the issue cursor's k-block (staged as k-block i_g): one elected lane
-  auto issue_kblock = [&]() {
-    if (i_in_chunk == 0) {
-      const uint32_t b = i_ch & 1;
-      wait(&tempty[b], ((i_ch >> 1) & 1) ^ 1);
-      fence_after_sync();
-      dcol = tmem_base + b * NMMA;
-    }
-    const uint32_t s = i_g % STAGES;
-    wait(&full[s], (i_g / STAGES) & 1);
-    fence_after_sync();
-    const uint32_t st = smem0 + s * Cfg::kStage;
-#pragma unroll
-    for (int a = 0; a < Cfg::kAtoms; ++a) {
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint32_t xs = st + a * Cfg::kXAtom + kk * 32;
-        const uint32_t ys = st + 2 * Cfg::kXPlane + a * Cfg::kYAtom + kk * 32;
-        const uint64_t x_big = umma_desc_sw128(xs);
-        const uint64_t x_small = umma_desc_sw128(xs + Cfg::kXPlane);
-        const uint64_t y_big = umma_desc_sw128(ys);
-        const uint64_t y_small = umma_desc_sw128(ys + Cfg::kYPlane);
-        const uint32_t acc0 = (i_in_chunk > 0 || a > 0 || kk > 0) ? 1u : 0u;
-        // small products first: accumulated before the big one
-        mma_tf32_elect(dcol, x_small, y_big, Cfg::kIdesc, acc0);
-        mma_tf32_elect(dcol, x_big, y_small, Cfg::kIdesc, 1u);
-        mma_tf32_elect(dcol, x_big, y_big, Cfg::kIdesc, 1u);
-      }
-    }
-    mma_commit_elect(&empty[s]);
-    ++i_g;
-    const bool unit_end = ic.kb + 1 == ic.kb_hi;
-    if (++i_in_chunk == p.chunk_kb || unit_end) {
-      mma_commit_elect(&tfull[i_ch & 1]);
-      ++i_ch;
-      i_in_chunk = 0;
-    }
-    ic.next(p);
-  };
   uint32_t staged = 0;
   while (true) {
     const uint32_t s0 = staged;
@@ -430,8 +441,10 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
       have_next = pc.valid();
       if (have_next) load(nx, ny);
     }
-    if (warp == 0) {
-      while (i_g < s0) issue_kblock();
+    if constexpr (!MW) {
+      if (warp == 0) {
+        while (i_g < s0) issue_kblock();
+      }
     }
     if (have) {
       const uint32_t s = s0 % STAGES;
@@ -544,6 +557,20 @@ __global__ void __launch_bounds__(kGtThreads, OCC) gather_tc_kernel(const __grid
       }
     }
     if (drain && !fc.valid()) break;
+  }
+  };  // worker_body
+  if constexpr (MW) {
+    if (warp >= kGtWorkerWarps) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 24;");
+      if (warp == kGtWorkerWarps) {  // the MMA warp: every k-block as soon as the workers have staged it
+        while (ic.valid()) issue_kblock();
+      }
+    } else {
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 240;");
+      worker_body();
+    }
+  } else {
+    worker_body();
   }
   fence_before_sync();
   __syncthreads();
@@ -1023,14 +1050,14 @@ void gather_tc_destroy(GatherTcPlan* plan) { delete plan; }
 
 namespace {
 
-template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC>
+template <int NMMA, int KBC, int STAGES, bool PX, bool PY, int OCC, bool MW = false>
 int launch_gt(const GtParams& p, int64_t units, double flops, double bytes, cudaStream_t stream) {
   using Cfg = GtCfg<NMMA, KBC, STAGES, PX, PY>;
-  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY, OCC>;
+  auto kern = gather_tc_kernel<NMMA, KBC, STAGES, PX, PY, OCC, MW>;
   TNC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(num_sms()) * OCC));
   ProfScope prof(PROF_TC_GATHER, flops, bytes, stream);
-  kern<<<grid, kGtThreads, Cfg::kSmem, stream>>>(p);
+  kern<<<grid, MW ? kGtThreads + 128 : kGtThreads, Cfg::kSmem, stream>>>(p);
   TNC_CHECK_LAUNCH();
   return TNC_OK;
 }
@@ -1071,9 +1098,15 @@ int gather_tc_launch(const GatherTcPlan* plan, const void* x, const void* y, voi
       TNC_GT_MODES(32, 32, 2);
     case 64: TNC_GT_MODES(64, 32, 2);
     case 128: TNC_GT_MODES(128, 16, 3);
-    case 256:
+    case 256: {
+      const char* mw_s = std::getenv("TNC_GT_MMAWARP");
+      if (!(mw_s && std::atoi(mw_s) == 0)) {
+        if (px) return launch_gt<256, 16, 2, true, false, 1, true>(p, units, flops, bytes, stream);
+        return launch_gt<256, 16, 2, false, false, 1, true>(p, units, flops, bytes, stream);
+      }
       if (px) return launch_gt<256, 16, 2, true, false, 1>(p, units, flops, bytes, stream);
       return launch_gt<256, 16, 2, false, false, 1>(p, units, flops, bytes, stream);
+    }
     default: TNC_RET(TNC_ERR_UNSUPPORTED, "tc_gather: bad tile width");
   }
 #undef TNC_GT_MODES
