@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(MW ? kGtThreads + 128 : kGtThreads, OCC) gathe
     while (fc.valid()) {
       const int64_t end = static_cast<int64_t>(f_c + 1) * p.chunk_kb;
       const int64_t last = static_cast<int64_t>(f_base) + (end < f_n ? end : f_n) - 1;
-      if (!drain && last + 2 > static_cast<int64_t>(s0)) break;
+      // (with the MMA warp a k-block's MMAs are issued as soon as it is staged: one iteration of slack is enough)
+      if (!drain && last + (MW ? 1 : 2) > static_cast<int64_t>(s0)) break;
       const uint32_t b = ch & 1;
       wait(&tfull[b], (ch >> 1) & 1);
       fence_after_sync();
