@@ -26,16 +26,20 @@
 //              splits: fp32 partials [split][row][col] (canonical order),
 //              then the fixed-order tree reduction
 //
-// Paired layout: when X's stride-1 leg is a common tile leg it sits on k bit
-// 0, so (k, k + 1) pairs are 16 contiguous bytes in HBM and in the swizzled
-// plane: one 16-byte load and one 16-byte store per plane move two elements
-// (Y likewise when the same leg is Y's stride-1 leg).
+// Pair stores: every X smem store moves a K-adjacent element pair, 16 bytes per
+// plane.  The pair leg sits on k bit 0; when it is X's stride-1 leg the pair
+// is also 16 contiguous bytes in HBM (memory pair: one 16-byte load, Y
+// likewise when it is Y's stride-1 leg too), otherwise it is the thread's
+// first iteration bit (register pair: two 8-byte loads, one 16-byte store).
 //
-// Roles (256 threads, 8 warps = 2 per SM sub-partition so each thread can
-// hold up to 255 registers): every warp gathers + splits (loads run one
-// k-block ahead of the smem stores), folds TMEM lane quadrant w % 4, column
-// half w / 4, and stores; warp 0 also owns TMEM and issues the MMAs of
-// k-block g-1 right after staging k-block g (one elected lane).
+// Roles.  256 worker threads (8 warps = 2 per SM sub-partition): every warp
+// gathers + splits (loads run one k-block ahead of the smem stores), folds
+// TMEM lane quadrant w % 4, column half w / 4, and stores.  MMA issue:
+//   * <= 128-column tiles: warp 0 issues the MMAs of k-block g-1 right after
+//     its loads of k-block g+1 (one elected lane); the narrowest tiles (<= 16
+//     columns) run two such CTAs per SM (16-K k-blocks, 128 registers);
+//   * 256-column tiles: a third warpgroup holds a dedicated MMA warp (384
+//     threads; setmaxnreg gives the workers 240 registers, that warpgroup 24).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
