@@ -692,6 +692,32 @@ int launch_tile(const PermPlan& pl, const void* in, void* out, const SplitOut& s
   return TNC_OK;
 }
 
+// Small tensors (the hundreds of leaf-sized steps of a slice): one thread per
+// output element decodes its index.  The tile kernel's per-block table setup
+// costs tens of microseconds, more than moving a megabyte.
+constexpr int64_t kSmallPermute = int64_t{1} << 17;
+struct SmallPermParams {
+  int rank;
+  int64_t total;
+  int64_t odim[TNC_MAX_RANK];     // output order, last fastest
+  int64_t istride[TNC_MAX_RANK];  // input stride of the same leg
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) permute_small_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                            const SmallPermParams p) {
+  const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= p.total) return;
+  int64_t rem = o, off = 0;
+  for (int a = p.rank - 1; a >= 0; --a) {
+    const int64_t d = p.odim[a];
+    const int64_t q = rem / d;
+    off += (rem - q * d) * p.istride[a];
+    rem = q;
+  }
+  out[o] = in[off];
+}
+
 int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_strides,
                    const int32_t* perm, const void* in, void* out, cudaStream_t stream) {
   const size_t eb = elem_bytes(dtype);
@@ -699,6 +725,22 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
   TNC_TRY(plan_permute(eb, rank, dims, in_strides, perm, pl));
   if (pl.kind == PermPlan::EMPTY) return TNC_OK;
   ProfScope prof(PROF_PERMUTE, 0.0, 2.0 * static_cast<double>(pl.total) * eb, stream);
+  if (pl.kind == PermPlan::TILE && pl.total <= kSmallPermute && std::getenv("TNC_NO_SMALL_PERMUTE") == nullptr) {
+    SmallPermParams sp;
+    sp.rank = rank;
+    sp.total = pl.total;
+    for (int t = 0; t < rank; ++t) {
+      sp.odim[t] = dims[perm[t]];
+      sp.istride[t] = in_strides[perm[t]];
+    }
+    const unsigned blocks = static_cast<unsigned>(ceil_div(pl.total, 256));
+    if (dtype == TNC_C128)
+      permute_small_kernel<c128><<<blocks, 256, 0, stream>>>(static_cast<const c128*>(in), static_cast<c128*>(out), sp);
+    else
+      permute_small_kernel<c64><<<blocks, 256, 0, stream>>>(static_cast<const c64*>(in), static_cast<c64*>(out), sp);
+    TNC_CHECK_LAUNCH();
+    return TNC_OK;
+  }
   if (pl.kind == PermPlan::MEMCPY) {
     TNC_CUDA_TRY(cudaMemcpyAsync(out, in, static_cast<size_t>(pl.total) * eb, cudaMemcpyDeviceToDevice, stream));
     return TNC_OK;
