@@ -699,8 +699,10 @@ constexpr int64_t kSmallPermute = int64_t{1} << 17;
 struct SmallPermParams {
   int rank;
   int64_t total;
+  int pow2;
   int64_t odim[TNC_MAX_RANK];     // output order, last fastest
   int64_t istride[TNC_MAX_RANK];  // input stride of the same leg
+  int olog[TNC_MAX_RANK];         // log2 of the extent when pow2
 };
 
 template <typename T>
@@ -709,11 +711,18 @@ __global__ void __launch_bounds__(256) permute_small_kernel(const T* __restrict_
   const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (o >= p.total) return;
   int64_t rem = o, off = 0;
-  for (int a = p.rank - 1; a >= 0; --a) {
-    const int64_t d = p.odim[a];
-    const int64_t q = rem / d;
-    off += (rem - q * d) * p.istride[a];
-    rem = q;
+  if (p.pow2) {  // every extent a power of two (qubit networks): shifts instead of divisions
+    for (int a = p.rank - 1; a >= 0; --a) {
+      off += (rem & (p.odim[a] - 1)) * p.istride[a];
+      rem >>= p.olog[a];
+    }
+  } else {
+    for (int a = p.rank - 1; a >= 0; --a) {
+      const int64_t d = p.odim[a];
+      const int64_t q = rem / d;
+      off += (rem - q * d) * p.istride[a];
+      rem = q;
+    }
   }
   out[o] = in[off];
 }
@@ -729,9 +738,14 @@ int permute_launch(int dtype, int rank, const int64_t* dims, const int64_t* in_s
     SmallPermParams sp;
     sp.rank = rank;
     sp.total = pl.total;
+    sp.pow2 = 1;
     for (int t = 0; t < rank; ++t) {
-      sp.odim[t] = dims[perm[t]];
+      const int64_t d = dims[perm[t]];
+      sp.odim[t] = d;
       sp.istride[t] = in_strides[perm[t]];
+      sp.olog[t] = 0;
+      while ((int64_t{1} << sp.olog[t]) < d) ++sp.olog[t];
+      if ((int64_t{1} << sp.olog[t]) != d) sp.pow2 = 0;
     }
     const unsigned blocks = static_cast<unsigned>(ceil_div(pl.total, 256));
     if (dtype == TNC_C128)
