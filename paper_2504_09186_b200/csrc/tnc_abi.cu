@@ -451,6 +451,7 @@ int tnc_init(int device) {
 // more than once; the library stays usable (tnc_init again).
 void tnc_shutdown(void) {
   tnc_profile_enable(0);
+  tnc::absorb_shutdown();
   cudaGetLastError();  // clear a sticky launch error from a failed call
 }
 

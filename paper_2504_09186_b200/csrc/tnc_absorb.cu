@@ -838,6 +838,15 @@ int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, 
   return TNC_OK;
 }
 
+// tnc_shutdown: drop the events that order streams on the constant table
+void absorb_shutdown() {
+  std::lock_guard<std::mutex> lock(g_const_mu);
+  for (ConstOwner& o : g_const_owner) {
+    if (o.done) cudaEventDestroy(o.done);
+    o = ConstOwner{};
+  }
+}
+
 int absorb_chain_passes(int t_rank, int n_gates, const int32_t* axes, int* passes, int* groups) {
   ChainPlan cp;
   TNC_TRY(plan_chain(t_rank, n_gates, axes, cp));

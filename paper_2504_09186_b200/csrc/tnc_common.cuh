@@ -205,6 +205,7 @@ int absorb_chain_workspace(int t_rank, int n_gates, const int32_t* axes, size_t*
 int absorb_chain_launch(int t_rank, const void* t_in, void* t_out, int n_gates, const void* const* gates,
                         const int64_t* gate_strides, const int32_t* axes, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream);
+void absorb_shutdown();
 int absorb_chain_passes(int t_rank, int n_gates, const int32_t* axes, int* passes, int* groups);
 
 }  // namespace tnc
